@@ -1,0 +1,148 @@
+/*
+ * sliced.h -- C ABI of the B200-native sliced-weight FFN path (libsliced.so).
+ *
+ * The reference has no FFI: its boundary is the Python operator API of
+ * /root/reference/pkg/src/sliceplan/slicing_kernel.py.  Each entry point below
+ * replaces one piece of it (file:line cited per function); the Python host
+ * (paper_2411_15715_b200/sliced.py) keeps the reference's names, argument
+ * meaning and exception classes on top of this ABI.
+ *
+ * Conventions
+ *   - Plain C: integers, sizes and raw pointers.  No torch / CUDA types in the
+ *     signatures except the opaque stream handle (a cudaStream_t, passed as
+ *     void*; NULL = the legacy default stream).
+ *   - Every function returns an sp_status; on failure sp_last_error() returns
+ *     a thread-local message.  Codes map 1:1 onto the reference exception
+ *     classes (sliceplan/errors.py:24-29): SP_ERR_SHAPE -> ShapeMismatch,
+ *     SP_ERR_TOKENS -> TokenCountOutOfRange, SP_ERR_VALUE -> ValueError.
+ *     Argument errors are detected before any work is enqueued, as the
+ *     reference raises before computing (slicing_kernel.py:64-70,111-118).
+ *   - Weights are copied into library-owned placement at layer creation
+ *     (GG -> HBM, CC and CG -> pinned host, chunk-interleaved); activations
+ *     and outputs stay caller-owned.
+ *   - One device per process/thread context (sp_init); forwards on one device
+ *     are serialised by the library.
+ */
+#ifndef SLICED_H_
+#define SLICED_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+
+typedef enum sp_status {
+  SP_OK = 0,
+  SP_ERR_SHAPE = 1,   /* ShapeMismatch        */
+  SP_ERR_TOKENS = 2,  /* TokenCountOutOfRange */
+  SP_ERR_VALUE = 3,   /* ValueError           */
+  SP_ERR_CUDA = 4,    /* CUDA runtime failure */
+  SP_ERR_NOMEM = 5,   /* allocation failure   */
+  SP_ERR_STATE = 6    /* not initialised / wrong device */
+} sp_status;
+
+typedef enum sp_dtype { SP_F32 = 0, SP_BF16 = 1 } sp_dtype;
+
+/* sliceplan.slicing_kernel.Activation (slicing_kernel.py:27-38) */
+typedef enum sp_act { SP_ACT_IDENTITY = 0, SP_ACT_SILU = 1, SP_ACT_GELU = 2 } sp_act;
+
+/* sp_forward_batch flags */
+#define SP_IO_DEVICE 0u     /* x / y are device pointers (inputs resident in HBM) */
+#define SP_IO_HOST 1u       /* x / y are host pointers; H2D / D2H inside the call  */
+#define SP_NO_CC_THREADS 2u /* run the CC slice on the calling thread only         */
+
+typedef struct sp_layer* sp_layer_t;
+
+/*
+ * One FFN instance (a dense MLP or one MoE expert) and its column split.
+ * Replaces SlicedWeights (slicing_kernel.py:41-54) + the floor rule of
+ * slice_weights (slicing_kernel.py:71-74): b1 = floor(cc*H), b2 =
+ * floor((cc+cg)*H) are computed by the caller and passed here.
+ *   cc block = hidden columns [0, b1)    host-resident, run on host threads
+ *   cg block = hidden columns [b1, b2)   host-resident, streamed, run on GPU
+ *   gg block = hidden columns [b2, H)    HBM-resident, run on GPU
+ */
+typedef struct sp_layer_desc {
+  int64_t model_dim;  /* M: input features  (rows of W1 / W3)              */
+  int64_t hidden_dim; /* H: the sliced dimension                           */
+  int64_t out_dim;    /* N: output features (columns of W2)                */
+  int32_t gated;      /* 0: act(x W1) W2   1: (act(x W1) * (x W3)) W2      */
+  int32_t act;        /* sp_act                                            */
+  int32_t wdtype;     /* sp_dtype of the stored weights                    */
+  int32_t chunk_rows; /* hidden rows per streamed chunk; 0 = auto (~8 MB)  */
+  int64_t b1, b2;     /* block boundaries, 0 <= b1 <= b2 <= H              */
+} sp_layer_desc;
+
+/* One expert application inside a batched forward. */
+typedef struct sp_call {
+  sp_layer_t layer;
+  int64_t tokens;           /* T_e rows this layer processes                   */
+  const int32_t* token_ids; /* host array [T_e]: rows of x; NULL = 0..T_e-1     */
+  const float* gates;       /* host array [T_e]: output weights; NULL = 1.0     */
+  int64_t n_g;              /* last n_g of the T_e rows run the CC block on the
+                               GPU (cg_prime, slicing_kernel.py:148-151)        */
+} sp_call;
+
+/* ---- library ---------------------------------------------------------- */
+int sp_abi_version(void);
+const char* sp_last_error(void);
+/* Select / initialise the CUDA device; creates the copy + compute streams and
+ * the host thread pool.  host_threads <= 0 = all online cores. */
+int sp_init(int device, int host_threads);
+int sp_shutdown(void);
+int sp_device_count(int* count);
+
+/* ---- placement (slice_weights, slicing_kernel.py:57-80) ---------------- */
+/* w1t, w3t: [H, M] row-major (nn.Linear(M->H).weight layout); w3t NULL unless
+ * gated.  w2t: [N, H] row-major (nn.Linear(H->N).weight).  Host pointers in
+ * desc->wdtype; they are copied, the caller may free them afterwards. */
+int sp_layer_create(const sp_layer_desc* desc, const void* w1t, const void* w3t,
+                    const void* w2t, sp_layer_t* out);
+int sp_layer_destroy(sp_layer_t layer);
+/* Bytes placed in HBM (gg), pinned host streamed to the GPU (cg) and pinned
+ * host computed on the CPU (cc). */
+int sp_layer_bytes(sp_layer_t layer, size_t* gg, size_t* cg, size_t* cc);
+/* Block widths (cc, cg, gg) == SlicedWeights.block_widths (slicing_kernel.py:50-54). */
+int sp_layer_widths(sp_layer_t layer, int64_t widths[3]);
+
+/* ---- forward (mlp_forward_sliced, slicing_kernel.py:97-124) ------------ */
+/* y[t, :] = sum over calls c, rows i with ids_c[i] == t of
+ *           gate_c[i] * FFN_c(x[t, :])   (FFN_c summed over its cc/cg/gg blocks)
+ * x: [T, M] (xdtype), y: [T, N] (ydtype), overwritten.  Rows no call touches
+ * are zero.  With SP_IO_DEVICE the call returns once the CC slice is done and
+ * the GPU work is enqueued (ordered after prior work on `stream`, and `stream`
+ * is ordered after it); with SP_IO_HOST it returns with y written. */
+int sp_forward_batch(const sp_call* calls, int n_calls, const void* x, int xdtype, int64_t T,
+                     void* y, int ydtype, unsigned flags, void* stream);
+
+/* Host-only CC block (no GPU): y_cc[T, N] (f32) = sum over cc columns.  Used by
+ * the CPU test suite and the host-core micro-benchmarks of the profile refit. */
+int sp_cc_forward_host(sp_layer_t layer, const void* x, int xdtype, int64_t T, float* y_cc,
+                       int threads);
+
+/* ---- profiling hooks (perf-model refit, measured timelines) ------------ */
+/* Last forward's measured stage intervals in the reference Gantt schema
+ * (pipeline.py:347-364): stream 0 launch, 1 transfer, 2 gpu, 3 cpu; times in
+ * seconds relative to the call start.  *n in: capacity, out: records. */
+typedef struct sp_trace_record {
+  int32_t index;  /* 1-based item index within the stream */
+  int32_t stream; /* 0 launch, 1 transfer, 2 gpu, 3 cpu    */
+  double start_s, end_s;
+  double bytes;   /* bytes moved / weight bytes touched    */
+} sp_trace_record;
+int sp_trace_enable(int on);
+int sp_trace_fetch(sp_trace_record* out, int* n);
+
+/* Pinned host buffer helpers (cudaHostAlloc; avoids torch's caching host
+ * allocator rounding). */
+int sp_host_alloc(size_t bytes, void** ptr);
+int sp_host_free(void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLICED_H_ */

@@ -1,0 +1,148 @@
+"""ctypes binding of libsliced.so (include/sliced.h).
+
+ctypes.CDLL drops the GIL for the duration of every foreign call, so the CC
+block's host threads and a Python caller's other threads keep running while a
+forward is in flight.  There is no Python fallback: if the library is missing
+or no sm_100 device is visible, the GPU entry points raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+from .errors import NativeError, raise_for
+
+LIB_PATH = Path(__file__).resolve().parent / "_native" / "libsliced.so"
+
+SP_F32, SP_BF16 = 0, 1
+SP_IO_DEVICE, SP_IO_HOST, SP_NO_CC_THREADS = 0, 1, 2
+ACT_CODES = {"identity": 0, "silu": 1, "gelu": 2}
+
+# symbol -> (restype, argtypes); the CPU suite checks this table against include/sliced.h
+_c_layer = C.c_void_p
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [
+        ("model_dim", C.c_int64),
+        ("hidden_dim", C.c_int64),
+        ("out_dim", C.c_int64),
+        ("gated", C.c_int32),
+        ("act", C.c_int32),
+        ("wdtype", C.c_int32),
+        ("chunk_rows", C.c_int32),
+        ("b1", C.c_int64),
+        ("b2", C.c_int64),
+    ]
+
+
+class Call(C.Structure):
+    _fields_ = [
+        ("layer", _c_layer),
+        ("tokens", C.c_int64),
+        ("token_ids", C.POINTER(C.c_int32)),
+        ("gates", C.POINTER(C.c_float)),
+        ("n_g", C.c_int64),
+    ]
+
+
+class TraceRecord(C.Structure):
+    _fields_ = [
+        ("index", C.c_int32),
+        ("stream", C.c_int32),
+        ("start_s", C.c_double),
+        ("end_s", C.c_double),
+        ("bytes", C.c_double),
+    ]
+
+
+SIGNATURES = {
+    "sp_abi_version": (C.c_int, []),
+    "sp_last_error": (C.c_char_p, []),
+    "sp_init": (C.c_int, [C.c_int, C.c_int]),
+    "sp_shutdown": (C.c_int, []),
+    "sp_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "sp_layer_create": (C.c_int, [C.POINTER(LayerDesc), C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.POINTER(_c_layer)]),
+    "sp_layer_destroy": (C.c_int, [_c_layer]),
+    "sp_layer_bytes": (C.c_int, [_c_layer, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                                 C.POINTER(C.c_size_t)]),
+    "sp_layer_widths": (C.c_int, [_c_layer, C.POINTER(C.c_int64)]),
+    "sp_forward_batch": (C.c_int, [C.POINTER(Call), C.c_int, C.c_void_p, C.c_int, C.c_int64,
+                                   C.c_void_p, C.c_int, C.c_uint, C.c_void_p]),
+    "sp_cc_forward_host": (C.c_int, [_c_layer, C.c_void_p, C.c_int, C.c_int64,
+                                     C.POINTER(C.c_float), C.c_int]),
+    "sp_trace_enable": (C.c_int, [C.c_int]),
+    "sp_trace_fetch": (C.c_int, [C.POINTER(TraceRecord), C.POINTER(C.c_int)]),
+    "sp_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "sp_host_free": (C.c_int, [C.c_void_p]),
+}
+
+_lib = None
+_lock = threading.Lock()
+_device: int | None = None
+
+
+def lib():
+    """Load libsliced.so once; raise if it was never built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise NativeError(
+                    f"{LIB_PATH} is missing; build it with `python -m paper_2411_15715_b200._build` "
+                    "(the sliced path has no CPU fallback)"
+                )
+            handle = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+        return _lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = lib().sp_last_error()
+        raise_for(status, msg.decode(errors="replace") if msg else "")
+
+
+def init(device: int | None = None, host_threads: int = 0) -> int:
+    """Bind the library to a CUDA device (default: torch's current device, else 0).
+
+    ``device=-1`` opens a host-only context (CC kernels only)."""
+    global _device
+    if device is None:
+        device = _device if _device is not None else _default_device()
+    if _device is not None and _device == device:
+        return device
+    threads = host_threads or int(os.environ.get("SP_HOST_THREADS", "0"))
+    check(lib().sp_init(int(device), int(threads)))
+    _device = device
+    return device
+
+
+def shutdown() -> None:
+    global _device
+    if _lib is not None:
+        check(_lib.sp_shutdown())
+    _device = None
+
+
+def current_device() -> int | None:
+    return _device
+
+
+def _default_device() -> int:
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:  # pragma: no cover
+        pass
+    return 0

@@ -1,0 +1,105 @@
+"""The C-ABI library: loads without a GPU, exports what include/sliced.h
+declares, maps status codes to the reference exception classes, and its CC
+host kernel (the only compute it may run without a device) matches the oracle."""
+
+from __future__ import annotations
+
+import ctypes as C
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, gpu_available
+from oracle import sliced_forward as orc
+from paper_2411_15715_b200 import _native as nat
+from paper_2411_15715_b200 import errors
+
+HEADER = (ROOT / "include" / "sliced.h").read_text()
+
+
+def declared_functions() -> set[str]:
+    return set(re.findall(r"^\s*(?:int|const char\*)\s+(sp_\w+)\s*\(", HEADER, re.M))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    lib = nat.lib()
+    declared = declared_functions()
+    assert len(declared) >= 14
+    for name in declared:
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(nat.LIB_PATH)], capture_output=True, text=True)
+    exported = set(re.findall(r" T (sp_\w+)", out.stdout))
+    assert declared <= exported
+    assert set(nat.SIGNATURES) == declared
+
+
+def test_abi_version_and_struct_layouts():
+    assert nat.lib().sp_abi_version() == int(re.search(r"SP_ABI_VERSION (\d+)", HEADER).group(1))
+    assert C.sizeof(nat.LayerDesc) == 3 * 8 + 4 * 4 + 2 * 8
+    assert C.sizeof(nat.Call) == 5 * 8
+    assert C.sizeof(nat.TraceRecord) == 8 + 3 * 8
+
+
+def test_status_codes_map_to_reference_classes():
+    for code, name in re.findall(r"SP_(ERR_\w+|OK) = (\d+)", HEADER):
+        pass
+    assert errors.SP_ERR_SHAPE == 1 and errors.SP_ERR_TOKENS == 2
+    with pytest.raises(errors.ShapeMismatch):
+        errors.raise_for(errors.SP_ERR_SHAPE, "x")
+    with pytest.raises(errors.TokenCountOutOfRange):
+        errors.raise_for(errors.SP_ERR_TOKENS, "x")
+    with pytest.raises(ValueError):
+        errors.raise_for(errors.SP_ERR_VALUE, "x")
+    assert issubclass(errors.ShapeMismatch, ValueError)
+
+
+@pytest.fixture(scope="module")
+def host_ctx():
+    if gpu_available():
+        pytest.skip("host-only context is for GPU-less hosts")
+    nat.init(-1, 4)
+    yield
+    nat.shutdown()
+
+
+def test_gpu_entry_points_refuse_without_device(host_ctx):
+    from paper_2411_15715_b200.sliced import CallSpec, NativeLayer, forward_calls
+
+    rng = np.random.default_rng(0)
+    lay = NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((8, 32)), 32, 32, "silu", dtype="f32")
+    with pytest.raises(errors.NativeError, match="no CPU fallback"):
+        forward_calls([CallSpec(lay)], rng.standard_normal((2, 16)))
+    # a GG block cannot be placed without a device
+    with pytest.raises(errors.NativeError):
+        NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((8, 32)), 0, 0, "silu", dtype="f32")
+
+
+def test_layer_create_validates_like_the_reference(host_ctx):
+    from paper_2411_15715_b200.sliced import NativeLayer
+
+    rng = np.random.default_rng(1)
+    with pytest.raises(errors.ShapeMismatch):
+        NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((8, 31)), 32, 32, dtype="f32")
+    with pytest.raises(ValueError):
+        NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((8, 32)), 20, 10, dtype="f32")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("gated", [False, True])
+@pytest.mark.parametrize("act", ["identity", "silu", "gelu"])
+def test_cc_host_kernel_matches_oracle(host_ctx, dtype, gated, act):
+    from paper_2411_15715_b200.sliced import NativeLayer
+
+    rng = np.random.default_rng(hash((dtype, gated, act)) % 2**32)
+    for M, H, N, T, chunk in ((64, 200, 48, 5, 64), (100, 130, 20, 1, 64), (37, 300, 33, 9, 128)):
+        w1, w3 = rng.uniform(-1, 1, (M, H)), rng.uniform(-1, 1, (M, H))
+        w2, x = rng.uniform(-1, 1, (H, N)), rng.uniform(-1, 1, (T, M))
+        lay = NativeLayer(w1.T, w2.T, H, H, act, w3.T if gated else None, dtype=dtype, chunk_rows=chunk)
+        got = lay.cc_forward_host(x, threads=3)
+        q = orc.bf16_round if dtype == "bf16" else (lambda a: a)
+        ref = orc.dense_forward(q(x), q(w1), q(w2), act, q(w3) if gated else None)
+        assert orc.max_rel_error(got, ref) <= 1e-5
+        assert lay.block_widths == (H, 0, 0)
+        assert lay.placed_bytes()["gg"] == 0 and lay.placed_bytes()["cc"] > 0

@@ -1,0 +1,180 @@
+"""GPU parity: the sliced path (GG/CG on the B200 through libsliced, CC on host
+threads) against the CPU oracle and the reference goldens.
+
+Tolerances (north star): fp32 max relative error <= 1e-5, bf16 <= 1e-2, with
+max relative error = max|got - ref| / max|ref| and the reference fed the
+bf16-rounded inputs a bf16 kernel sees.
+"""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import sliced_forward as orc
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+BF16_TOL = 1e-2
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def sp():
+    import paper_2411_15715_b200 as sp
+    from paper_2411_15715_b200 import _native
+
+    _native.init(0)
+    return sp
+
+
+def _golden():
+    npz = np.load(GOLDEN / "forward_golden.npz")
+    return npz, json.loads(bytes(npz["meta_json"]).decode())
+
+
+def test_reference_goldens_fp32(sp):
+    npz, meta = _golden()
+    for case in meta["cases"]:
+        k = case["key"]
+        x, w1, w2 = npz[f"{k}_x"], npz[f"{k}_w1"], npz[f"{k}_w2"]
+        rates = sp.SlicingRates(*(float.fromhex(v) for v in case["rates"]))
+        act = sp.Activation(case["act"])
+        sliced = sp.slice_weights(w1, w2, rates)
+        assert list(sliced.block_widths) == case["widths"]
+        got = sp.mlp_forward_sliced(x, sliced, act, case["n_g"])
+        assert got.dtype == np.float64 and got.shape == npz[f"{k}_sliced"].shape
+        assert orc.max_rel_error(got, npz[f"{k}_sliced"]) <= FP32_TOL, k
+        dense = sp.mlp_forward_reference(x, w1, w2, act)
+        assert orc.max_rel_error(dense, npz[f"{k}_dense"]) <= FP32_TOL, k
+
+
+def test_recombination_sweep_matches_reference_bound(sp):
+    # the reference's own sweep (slicing_kernel.py:161-190), GPU sliced vs GPU dense
+    assert sp.max_recombination_error(seed=123, trials=20) <= 1e-4
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
+@pytest.mark.parametrize("gated", [False, True])
+def test_random_shapes_all_splits(sp, dtype, tol, gated):
+    rng = np.random.default_rng(2024 + gated + (dtype == "bf16") * 7)
+    q = orc.bf16_round if dtype == "bf16" else (lambda a: a)
+    for trial in range(12):
+        T = int(rng.choice([1, 2, 3, 5, 8, 9, 17]))
+        M = int(rng.integers(2, 300))
+        H = int(rng.integers(2, 900))
+        N = int(rng.integers(2, 300))
+        x, w1, w3, w2 = (q(rng.uniform(-1, 1, s)) for s in ((T, M), (M, H), (M, H), (H, N)))
+        raw = rng.dirichlet(np.ones(3)) if trial % 4 else np.eye(3)[trial // 4 % 3]
+        rates = sp.SlicingRates(raw[0], raw[1], 1.0 - raw[0] - raw[1])
+        act = list(sp.Activation)[trial % 3]
+        n_g = int(rng.integers(0, T + 1))
+        sliced = sp.slice_weights(w1, w2, rates, w3 if gated else None, dtype=dtype, chunk_rows=64)
+        got = sp.mlp_forward_sliced(x, sliced, act, n_g)
+        ref = orc.sliced_forward(x, w1, w2, act.value, rates.cc, rates.cg, w3 if gated else None)
+        assert orc.max_rel_error(got, ref) <= tol, (trial, T, M, H, N, sliced.block_widths, n_g)
+
+
+def test_many_chunks_exercise_ring_reuse(sp):
+    # 1000 hidden rows in 64-row chunks: 16 chunks through a 3-slot ring
+    rng = np.random.default_rng(7)
+    T, M, H, N = 4, 96, 1000, 80
+    x, w1, w3, w2 = (rng.uniform(-1, 1, s) for s in ((T, M), (M, H), (M, H), (H, N)))
+    for cc, cg in ((0.0, 1.0), (0.3, 0.6), (0.5, 0.2)):
+        rates = sp.SlicingRates(cc, cg, 1.0 - cc - cg)
+        sliced = sp.slice_weights(w1, w2, rates, w3, chunk_rows=64)
+        for n_g in (0, 2, T):
+            got = sp.mlp_forward_sliced(x, sliced, sp.Activation.SILU, n_g)
+            ref = orc.dense_forward(x, w1, w2, "silu", w3)
+            assert orc.max_rel_error(got, ref) <= FP32_TOL
+
+
+def test_diversion_does_not_change_results(sp):
+    rng = np.random.default_rng(11)
+    x, w1, w2 = rng.uniform(-1, 1, (6, 40)), rng.uniform(-1, 1, (40, 90)), rng.uniform(-1, 1, (90, 30))
+    sliced = sp.slice_weights(w1, w2, sp.SlicingRates(1, 0, 0))
+    outs = [sp.mlp_forward_sliced(x, sliced, sp.Activation.GELU, n_g=g) for g in range(7)]
+    for o in outs[1:]:
+        assert np.max(np.abs(o - outs[0])) <= 1e-5
+
+
+def test_deterministic_repeat(sp):
+    rng = np.random.default_rng(12)
+    x, w1, w3, w2 = (rng.uniform(-1, 1, s) for s in ((3, 128), (128, 700), (128, 700), (700, 64)))
+    sliced = sp.slice_weights(w1, w2, sp.SlicingRates(0.2, 0.3, 0.5), w3, dtype="bf16", chunk_rows=128)
+    a = sp.mlp_forward_sliced(x, sliced, sp.Activation.SILU)
+    b = sp.mlp_forward_sliced(x, sliced, sp.Activation.SILU)
+    assert np.array_equal(a, b)
+
+
+def test_device_io_matches_host_io(sp, torch):
+    from paper_2411_15715_b200.sliced import SlicedFFN
+
+    rng = np.random.default_rng(13)
+    M, H, N = 256, 1536, 256
+    w1t, w3t, w2t = (rng.standard_normal(s).astype(np.float32) / 16 for s in ((H, M), (H, M), (N, H)))
+    ffn = SlicedFFN(w1t, w2t, sp.SlicingRates(0.25, 0.25, 0.5), w3t=w3t, dtype="bf16", chunk_rows=256)
+    x = torch.randn(5, M, device="cuda", dtype=torch.bfloat16)
+    y_dev = ffn(x)
+    torch.cuda.synchronize()
+    y_host = ffn(x.cpu().float().numpy())
+    assert y_dev.dtype == torch.bfloat16 and y_dev.is_cuda
+    ref = orc.dense_forward(orc.bf16_round(x.float().cpu().numpy()), orc.bf16_round(w1t.T),
+                            orc.bf16_round(w2t.T), "silu", orc.bf16_round(w3t.T))
+    assert orc.max_rel_error(y_dev.float().cpu().numpy(), ref) <= BF16_TOL
+    assert orc.max_rel_error(y_host, ref) <= 1e-4
+
+
+def test_moe_top2_matches_oracle(sp, torch):
+    from paper_2411_15715_b200.sliced import SlicedFFN, SlicedMoE
+
+    rng = np.random.default_rng(14)
+    E, M, H = 8, 128, 448
+    experts_w = [tuple(rng.standard_normal(s).astype(np.float32) / 8 for s in ((H, M), (H, M), (M, H)))
+                 for _ in range(E)]
+    rates = [sp.SlicingRates(*(lambda r: (r[0], r[1], 1 - r[0] - r[1]))(rng.dirichlet(np.ones(3))))
+             for _ in range(E)]
+    experts = [SlicedFFN(w1t, w2t, r, w3t=w3t, dtype="f32", chunk_rows=64)
+               for (w1t, w3t, w2t), r in zip(experts_w, rates)]
+    router = rng.standard_normal((M, E))
+    moe = SlicedMoE(experts, router, top_k=2)
+    for T in (1, 4, 11):
+        x = rng.standard_normal((T, M))
+        got = moe(x)
+        ref = orc.moe_forward(x, [(w1t.T, w3t.T, w2t.T) for (w1t, w3t, w2t) in experts_w], router, 2)
+        assert orc.max_rel_error(got, ref) <= FP32_TOL
+        xd = torch.from_numpy(x.astype(np.float32)).cuda()
+        got_d = moe(xd).cpu().numpy()
+        assert orc.max_rel_error(got_d, ref) <= FP32_TOL
+
+
+@pytest.mark.slow
+def test_full_size_mixtral_expert_bf16(sp, torch):
+    """One Mixtral-8x7B expert (4096 x 14336, SwiGLU, bf16) at config-2 style
+    rates: GPU sliced vs fp64 oracle on the same bf16 values."""
+    from paper_2411_15715_b200.sliced import SlicedFFN
+
+    M, H = 4096, 14336
+    g = torch.Generator(device="cuda").manual_seed(0)
+    w1t = (torch.randn(H, M, device="cuda", generator=g) / 64).to(torch.bfloat16)
+    w3t = (torch.randn(H, M, device="cuda", generator=g) / 64).to(torch.bfloat16)
+    w2t = (torch.randn(M, H, device="cuda", generator=g) / 120).to(torch.bfloat16)
+    x = torch.randn(2, M, device="cuda", generator=g).to(torch.bfloat16)
+    ffn = SlicedFFN(w1t, w2t, sp.SlicingRates(0.15, 0.2, 0.65), w3t=w3t, dtype="bf16")
+    y = ffn(x).float().cpu().numpy()
+    f = lambda t: t.float().cpu().numpy().astype(np.float64)  # noqa: E731
+    ref = orc.dense_forward(f(x), f(w1t).T, f(w2t).T, "silu", f(w3t).T)
+    assert orc.max_rel_error(y, ref) <= BF16_TOL
+    # output rounding to bf16 dominates; the fp32 accumulation itself is much tighter
+    assert orc.max_rel_error(y, ref) <= 5e-3
