@@ -128,14 +128,29 @@ int sp_cc_forward_host(sp_layer_t layer, const void* x, int xdtype, int64_t T, f
 /* Last forward's measured stage intervals in the reference Gantt schema
  * (pipeline.py:347-364): stream 0 launch, 1 transfer, 2 gpu, 3 cpu; times in
  * seconds relative to the call start.  *n in: capacity, out: records. */
+typedef enum sp_trace_kind {
+  SP_TRACE_LAUNCH = 0,   /* host: enqueue of one forward's GPU work        */
+  SP_TRACE_GG = 1,       /* gpu: GG up + down kernels of one call          */
+  SP_TRACE_CG = 2,       /* gpu: one streamed CG chunk's kernels           */
+  SP_TRACE_CG_PRIME = 3, /* gpu: one streamed CC chunk for the n_g rows    */
+  SP_TRACE_COPY = 4,     /* transfer: one chunk's host-to-device copy      */
+  SP_TRACE_CC = 5,       /* cpu: CC block of one call on host threads      */
+  SP_TRACE_MERGE = 6     /* gpu: merge kernel                              */
+} sp_trace_kind;
 typedef struct sp_trace_record {
-  int32_t index;  /* 1-based item index within the stream */
-  int32_t stream; /* 0 launch, 1 transfer, 2 gpu, 3 cpu    */
+  int32_t index;  /* 1-based item index within its stream                */
+  int32_t stream; /* 0 launch, 1 transfer, 2 gpu, 3 cpu (pipeline.py:264) */
+  int32_t kind;   /* sp_trace_kind                                        */
+  int32_t call;   /* forward sequence number since sp_trace_enable        */
   double start_s, end_s;
-  double bytes;   /* bytes moved / weight bytes touched    */
+  double bytes;   /* weight bytes moved or touched                        */
 } sp_trace_record;
+/* on != 0 clears the trace and starts recording (events on the library's own
+ * streams, host clock for CC); sp_trace_fetch synchronises the device. */
 int sp_trace_enable(int on);
 int sp_trace_fetch(sp_trace_record* out, int* n);
+/* Kernels launched and bytes copied host-to-device by the library so far. */
+int sp_stats(uint64_t* kernel_launches, uint64_t* h2d_bytes);
 
 /* Pinned host buffer helpers (cudaHostAlloc; avoids torch's caching host
  * allocator rounding). */

@@ -20,6 +20,8 @@ LIB_PATH = Path(__file__).resolve().parent / "_native" / "libsliced.so"
 SP_F32, SP_BF16 = 0, 1
 SP_IO_DEVICE, SP_IO_HOST, SP_NO_CC_THREADS = 0, 1, 2
 ACT_CODES = {"identity": 0, "silu": 1, "gelu": 2}
+TRACE_KINDS = ("launch", "gg", "cg", "cg_prime", "copy", "cc", "merge")
+STREAM_NAMES = ("launch", "transfer", "gpu", "cpu")
 
 # symbol -> (restype, argtypes); the CPU suite checks this table against include/sliced.h
 _c_layer = C.c_void_p
@@ -53,6 +55,8 @@ class TraceRecord(C.Structure):
     _fields_ = [
         ("index", C.c_int32),
         ("stream", C.c_int32),
+        ("kind", C.c_int32),
+        ("call", C.c_int32),
         ("start_s", C.c_double),
         ("end_s", C.c_double),
         ("bytes", C.c_double),
@@ -77,6 +81,7 @@ SIGNATURES = {
                                      C.POINTER(C.c_float), C.c_int]),
     "sp_trace_enable": (C.c_int, [C.c_int]),
     "sp_trace_fetch": (C.c_int, [C.POINTER(TraceRecord), C.POINTER(C.c_int)]),
+    "sp_stats": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "sp_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "sp_host_free": (C.c_int, [C.c_void_p]),
 }
@@ -146,3 +151,27 @@ def _default_device() -> int:
     except Exception:  # pragma: no cover
         pass
     return 0
+
+
+def trace_enable(on: bool = True) -> None:
+    check(lib().sp_trace_enable(1 if on else 0))
+
+
+def trace_fetch() -> list[dict]:
+    """Measured spans since trace_enable, in the reference Gantt schema
+    (pipeline.py:347-364) plus ``kind`` / ``call`` / ``bytes``."""
+    n = C.c_int(0)
+    check(lib().sp_trace_fetch(None, C.byref(n)))
+    buf = (TraceRecord * max(1, n.value))()
+    check(lib().sp_trace_fetch(buf, C.byref(n)))
+    return [
+        {"gemm_index": r.index, "stream": STREAM_NAMES[r.stream], "start_s": r.start_s,
+         "end_s": r.end_s, "kind": TRACE_KINDS[r.kind], "call": r.call, "bytes": r.bytes}
+        for r in buf[: n.value]
+    ]
+
+
+def stats() -> dict:
+    launches, h2d = C.c_uint64(), C.c_uint64()
+    check(lib().sp_stats(C.byref(launches), C.byref(h2d)))
+    return {"kernel_launches": launches.value, "h2d_bytes": h2d.value}

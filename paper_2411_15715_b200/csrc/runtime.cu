@@ -101,9 +101,21 @@ struct PinnedBuf {
 
 constexpr int kRingSlots = 3;
 
+// Measured timeline: CUDA events on the library's streams (GPU spans) and the
+// host clock (launch / CC spans), both relative to one synchronised origin.
+struct Span {
+  cudaEvent_t a = nullptr, b = nullptr;  // GPU span
+  double ha = 0, hb = 0;                 // host span (seconds since host_t0)
+  int stream, kind, call;
+  double bytes;
+};
 struct Trace {
   bool on = false;
-  std::vector<sp_trace_record> recs;
+  cudaEvent_t t0 = nullptr;
+  double host_t0 = 0;
+  int call = 0;
+  std::vector<Span> spans;
+  std::vector<cudaEvent_t> pool;
 };
 
 struct Context {
@@ -124,6 +136,7 @@ struct Context {
   std::mutex mu;
   Trace trace;
   std::map<std::pair<const void*, size_t>, int> occ_cache;
+  uint64_t launches = 0, h2d_bytes = 0;
 };
 
 static std::mutex g_ctx_mu;
@@ -280,6 +293,7 @@ static int launch_rowdot_t(Context* C, const RowDotArgs& a, cudaStream_t s) {
   const size_t smem = (fixed + size_t(per_cta) * G * TT) * sizeof(float);
   kern<<<grid, kThreads, smem, s>>>(a);
   SP_CUDA(cudaGetLastError());
+  ++C->launches;
   return SP_OK;
 }
 
@@ -384,6 +398,54 @@ static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+static cudaEvent_t trace_event(Context* C) {
+  if (!C->trace.pool.empty()) {
+    cudaEvent_t e = C->trace.pool.back();
+    C->trace.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// GPU span bracketing the work enqueued on `s` between begin and end.
+struct GpuSpan {
+  Context* C;
+  cudaStream_t s;
+  Span sp;
+  bool on;
+  GpuSpan(Context* c, cudaStream_t st, int stream, int kind, double bytes)
+      : C(c), s(st), on(c->trace.on) {
+    if (!on) return;
+    sp.stream = stream;
+    sp.kind = kind;
+    sp.call = c->trace.call;
+    sp.bytes = bytes;
+    sp.a = trace_event(C);
+    sp.b = trace_event(C);
+    cudaEventRecord(sp.a, s);
+  }
+  void end() {
+    if (!on) return;
+    cudaEventRecord(sp.b, s);
+    C->trace.spans.push_back(sp);
+    on = false;
+  }
+};
+
+static void host_span(Context* C, int stream, int kind, double a, double b, double bytes) {
+  if (!C->trace.on) return;
+  Span sp;
+  sp.stream = stream;
+  sp.kind = kind;
+  sp.call = C->trace.call;
+  sp.bytes = bytes;
+  sp.ha = a - C->trace.host_t0;
+  sp.hb = b - C->trace.host_t0;
+  C->trace.spans.push_back(sp);
+}
+
 // ---------------------------------------------------------------------------
 // forward
 
@@ -426,8 +488,6 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   if (n_calls == 0) return fail(SP_ERR_VALUE, "sp_forward_batch needs at least one call");
   const bool host_io = flags & SP_IO_HOST;
   const double t_call = now_s();
-  auto& tr = C->trace;
-  tr.recs.clear();
 
   // ---- workspace layout ----
   const size_t xel = xdtype == SP_BF16 ? 2 : 4, yel = ydtype == SP_BF16 ? 2 : 4;
@@ -527,7 +587,9 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     if (L->h_gg > 0) {
       BlockView b{static_cast<const char*>(L->gg), L->gg_w3_off, L->gg_w2_off, L->h_gg, L->ldm,
                   L->ld_gg, L->d.b2};
+      GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, double(L->gg_bytes));
       SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], 0, Te, false, C->s_comp));
+      span.end();
     } else {
       SP_CUDA(cudaMemsetAsync(ws[c].y, 0, size_t(Te) * N * 4, C->s_comp));
     }
@@ -547,24 +609,34 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       const int slot = C->ring_next;
       C->ring_next = (C->ring_next + 1) % kRingSlots;
       SP_CUDA(cudaStreamWaitEvent(C->s_copy, C->ev_free[slot], 0));
-      SP_CUDA(cudaMemcpyAsync(C->ring[slot].p, static_cast<const char*>(L->host) + ch.off, ch.bytes,
-                              cudaMemcpyHostToDevice, C->s_copy));
+      {
+        GpuSpan span(C, C->s_copy, 1, SP_TRACE_COPY, double(ch.bytes));
+        SP_CUDA(cudaMemcpyAsync(C->ring[slot].p, static_cast<const char*>(L->host) + ch.off,
+                                ch.bytes, cudaMemcpyHostToDevice, C->s_copy));
+        span.end();
+      }
+      C->h2d_bytes += ch.bytes;
       SP_CUDA(cudaEventRecord(C->ev_copied[slot], C->s_copy));
       SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_copied[slot], 0));
       BlockView b{static_cast<const char*>(C->ring[slot].p), ch.w3_off, ch.w2_off, ch.rc, L->ldm,
                   ch.ldc, ch.r0};
       const int t0 = is_cc ? Te - ng : 0;
-      SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], t0, Te - t0, true, C->s_comp));
+      {
+        GpuSpan span(C, C->s_comp, 2, is_cc ? SP_TRACE_CG_PRIME : SP_TRACE_CG, double(ch.bytes));
+        SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], t0, Te - t0, true, C->s_comp));
+        span.end();
+      }
       SP_CUDA(cudaEventRecord(C->ev_free[slot], C->s_comp));
       ++chunk_seq;
     }
   }
 
   // ---- CC block on host threads (overlaps everything enqueued above) ----
-  const double t_cc0 = now_s();
+  host_span(C, 0, SP_TRACE_LAUNCH, t_call, now_s(), 0.0);
   if (need_cc) {
     if (!host_io) SP_CUDA(cudaEventSynchronize(C->ev_x));
     for (int c = 0; c < n_calls; ++c) {
+      const double t_cc0 = now_s();
       const sp_layer* L = calls[c].layer;
       const int64_t Tcc = calls[c].tokens - calls[c].n_g;
       if (L->d.b1 <= 0 || Tcc <= 0) continue;
@@ -595,13 +667,13 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
                    L->d.b1, xh, ldx, Tcc, ah, lda,
                    reinterpret_cast<float*>(hp + p_ycc[c])};
       cc_forward(pr, *C->pool, (flags & SP_NO_CC_THREADS) ? 1 : C->host_threads);
+      host_span(C, 3, SP_TRACE_CC, t_cc0, now_s(), double(L->cc_bytes));
       SP_CUDA(cudaMemcpyAsync(ws[c].ycc, hp + p_ycc[c], size_t(Tcc) * N * 4, cudaMemcpyHostToDevice,
                               C->s_aux));
     }
     SP_CUDA(cudaEventRecord(C->ev_ycc, C->s_aux));
     SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_ycc, 0));
   }
-  const double t_cc1 = now_s();
 
   // ---- merge ----
   MergeArgs ma{};
@@ -621,8 +693,11 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   {
     const int threads = 256;
     const int blocks = int(std::min<int64_t>((N + threads - 1) / threads, int64_t(C->num_sms) * 4));
+    GpuSpan span(C, C->s_comp, 2, SP_TRACE_MERGE, 0.0);
     merge_kernel<<<blocks, threads, 0, C->s_comp>>>(ma);
     SP_CUDA(cudaGetLastError());
+    span.end();
+    ++C->launches;
   }
   if (host_io) {
     SP_CUDA(cudaMemcpyAsync(hp + p_y, dws + o_ydev, size_t(T) * N * yel, cudaMemcpyDeviceToHost,
@@ -633,10 +708,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     SP_CUDA(cudaEventRecord(C->ev_done, C->s_comp));
     SP_CUDA(cudaStreamWaitEvent(user, C->ev_done, 0));
   }
-  if (tr.on) {
-    sp_trace_record r{1, 3, t_cc0 - t_call, t_cc1 - t_call, double(0)};
-    tr.recs.push_back(r);
-  }
+  if (C->trace.on) ++C->trace.call;
   (void)chunk_seq;
   return SP_OK;
 }
@@ -853,19 +925,69 @@ int sp_cc_forward_host(sp_layer_t L, const void* x, int xdtype, int64_t T, float
 
 int sp_trace_enable(int on) {
   Context* C = ctx_or_null();
-  if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
-  C->trace.on = on != 0;
+  if (!C || C->host_only) return fail(SP_ERR_STATE, "sp_init(device) has not been called");
+  std::lock_guard<std::mutex> g(C->mu);
+  Trace& tr = C->trace;
+  SP_CUDA(cudaDeviceSynchronize());
+  for (Span& sp : tr.spans) {
+    if (sp.a) tr.pool.push_back(sp.a);
+    if (sp.b) tr.pool.push_back(sp.b);
+  }
+  tr.spans.clear();
+  tr.call = 0;
+  tr.on = on != 0;
+  if (tr.on) {
+    if (!tr.t0) SP_CUDA(cudaEventCreate(&tr.t0));
+    SP_CUDA(cudaEventRecord(tr.t0, C->s_comp));
+    SP_CUDA(cudaEventSynchronize(tr.t0));
+    tr.host_t0 = now_s();
+  }
   return SP_OK;
 }
 
 int sp_trace_fetch(sp_trace_record* out, int* n) {
   Context* C = ctx_or_null();
-  if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  if (!C || C->host_only) return fail(SP_ERR_STATE, "sp_init(device) has not been called");
   if (!n) return fail(SP_ERR_VALUE, "n is NULL");
-  const int have = int(C->trace.recs.size());
-  const int k = out ? std::min(*n, have) : 0;
-  for (int i = 0; i < k; ++i) out[i] = C->trace.recs[i];
-  *n = out ? k : have;
+  std::lock_guard<std::mutex> g(C->mu);
+  Trace& tr = C->trace;
+  const int have = int(tr.spans.size());
+  if (!out) {
+    *n = have;
+    return SP_OK;
+  }
+  SP_CUDA(cudaDeviceSynchronize());
+  const int k = std::min(*n, have);
+  int counters[4] = {0, 0, 0, 0};
+  for (int i = 0; i < k; ++i) {
+    const Span& sp = tr.spans[i];
+    sp_trace_record r{};
+    r.index = ++counters[sp.stream & 3];
+    r.stream = sp.stream;
+    r.kind = sp.kind;
+    r.call = sp.call;
+    r.bytes = sp.bytes;
+    if (sp.a) {
+      float ma = 0, mb = 0;
+      SP_CUDA(cudaEventElapsedTime(&ma, tr.t0, sp.a));
+      SP_CUDA(cudaEventElapsedTime(&mb, tr.t0, sp.b));
+      r.start_s = ma * 1e-3;
+      r.end_s = mb * 1e-3;
+    } else {
+      r.start_s = sp.ha;
+      r.end_s = sp.hb;
+    }
+    out[i] = r;
+  }
+  *n = k;
+  return SP_OK;
+}
+
+int sp_stats(uint64_t* kernel_launches, uint64_t* h2d_bytes) {
+  Context* C = ctx_or_null();
+  if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  if (kernel_launches) *kernel_launches = C->launches;
+  if (h2d_bytes) *h2d_bytes = C->h2d_bytes;
   return SP_OK;
 }
 

@@ -39,12 +39,12 @@ def test_abi_version_and_struct_layouts():
     assert nat.lib().sp_abi_version() == int(re.search(r"SP_ABI_VERSION (\d+)", HEADER).group(1))
     assert C.sizeof(nat.LayerDesc) == 3 * 8 + 4 * 4 + 2 * 8
     assert C.sizeof(nat.Call) == 5 * 8
-    assert C.sizeof(nat.TraceRecord) == 8 + 3 * 8
+    assert C.sizeof(nat.TraceRecord) == 4 * 4 + 3 * 8
 
 
 def test_status_codes_map_to_reference_classes():
-    for code, name in re.findall(r"SP_(ERR_\w+|OK) = (\d+)", HEADER):
-        pass
+    codes = dict(re.findall(r"SP_(ERR_\w+|OK) = (\d+)", HEADER))
+    assert int(codes["ERR_SHAPE"]) == errors.SP_ERR_SHAPE and int(codes["ERR_TOKENS"]) == errors.SP_ERR_TOKENS
     assert errors.SP_ERR_SHAPE == 1 and errors.SP_ERR_TOKENS == 2
     with pytest.raises(errors.ShapeMismatch):
         errors.raise_for(errors.SP_ERR_SHAPE, "x")
@@ -92,7 +92,7 @@ def test_layer_create_validates_like_the_reference(host_ctx):
 def test_cc_host_kernel_matches_oracle(host_ctx, dtype, gated, act):
     from paper_2411_15715_b200.sliced import NativeLayer
 
-    rng = np.random.default_rng(hash((dtype, gated, act)) % 2**32)
+    rng = np.random.default_rng([len(dtype), int(gated), len(act)])
     for M, H, N, T, chunk in ((64, 200, 48, 5, 64), (100, 130, 20, 1, 64), (37, 300, 33, 9, 128)):
         w1, w3 = rng.uniform(-1, 1, (M, H)), rng.uniform(-1, 1, (M, H))
         w2, x = rng.uniform(-1, 1, (H, N)), rng.uniform(-1, 1, (T, M))
