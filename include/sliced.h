@@ -97,11 +97,13 @@ int sp_shutdown(void);
 int sp_device_count(int* count);
 
 /* ---- placement (slice_weights, slicing_kernel.py:57-80) ---------------- */
-/* w1t, w3t: [H, M] row-major (nn.Linear(M->H).weight layout); w3t NULL unless
- * gated.  w2t: [N, H] row-major (nn.Linear(H->N).weight).  Host pointers in
- * desc->wdtype; they are copied, the caller may free them afterwards. */
+/* w1t, w3t: [H, M] row-major (nn.Linear(M->H).weight layout, i.e. the
+ * reference's w1 transposed); w3t NULL unless gated.  w2: [H, N] row-major (the
+ * reference's own w2 layout, slicing_kernel.py:77).  Hidden unit h then owns
+ * row h of all three, so every block is a contiguous row range.  Host pointers
+ * in desc->wdtype; they are copied, the caller may free them afterwards. */
 int sp_layer_create(const sp_layer_desc* desc, const void* w1t, const void* w3t,
-                    const void* w2t, sp_layer_t* out);
+                    const void* w2, sp_layer_t* out);
 int sp_layer_destroy(sp_layer_t layer);
 /* Bytes placed in HBM (gg), pinned host streamed to the GPU (cg) and pinned
  * host computed on the CPU (cc). */

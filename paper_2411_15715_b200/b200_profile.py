@@ -11,7 +11,8 @@ runtime executes on, through the runtime's own code paths:
   between samples so the weights stream from HBM as they do in decode.
 * ``cpu_gemm_fp16`` -- the CC block on the host thread pool (AVX-512), per
   GEMM = wall time / 3; n = T * M * h.  The L3 is flushed between samples.
-* ``c2g``           -- pinned host -> HBM copies of n bytes on one stream.
+* ``c2g``           -- the runtime's own pinned-host -> HBM chunk copies (copy
+  stream trace spans) over chunk sizes 0.8 - 31 MB.
 * ``launch``        -- host enqueue time per kernel launch of a forward.
 
 ``python -m paper_2411_15715_b200.b200_profile --out profiles/`` writes the
@@ -65,7 +66,7 @@ def gpu_gemm_samples(torch, tokens: int, widths, model_dim=4096, reps=5, seed=0)
         w1t = (torch.randn(h, model_dim, device="cuda", generator=g) / 64).to(torch.bfloat16).cpu()
         w3t = (torch.randn(h, model_dim, device="cuda", generator=g) / 64).to(torch.bfloat16).cpu()
         w2t = (torch.randn(model_dim, h, device="cuda", generator=g) / 64).to(torch.bfloat16).cpu()
-        lay = NativeLayer(w1t, w2t, 0, 0, "silu", w3t, dtype="bf16")
+        lay = NativeLayer(w1t, w2t.t().contiguous(), 0, 0, "silu", w3t, dtype="bf16")
         x = torch.randn(tokens, model_dim, device="cuda").to(torch.bfloat16)
         from .sliced import CallSpec, forward_calls
 
@@ -92,8 +93,8 @@ def cpu_gemm_samples(tokens: int, widths, model_dim=4096, reps=5, seed=0, thread
     for h in widths:
         w1t = (rng.standard_normal((h, model_dim), dtype=np.float32) / 64)
         w3t = (rng.standard_normal((h, model_dim), dtype=np.float32) / 64)
-        w2t = (rng.standard_normal((model_dim, h), dtype=np.float32) / 64)
-        lay = NativeLayer(w1t, w2t, h, h, "silu", w3t, dtype="bf16")
+        w2 = (rng.standard_normal((h, model_dim), dtype=np.float32) / 64)
+        lay = NativeLayer(w1t, w2, h, h, "silu", w3t, dtype="bf16")
         x = rng.standard_normal((tokens, model_dim))
         for r in range(reps + 1):
             _flush_host(flush)
@@ -106,20 +107,28 @@ def cpu_gemm_samples(tokens: int, widths, model_dim=4096, reps=5, seed=0, thread
     return out
 
 
-def c2g_samples(torch, sizes, reps=5):
+def c2g_samples(torch, chunk_rows=(32, 64, 128, 320, 640, 1280), reps=3, model_dim=4096):
+    """Host-to-HBM chunk copies of the runtime itself (cudaHostAlloc'd region,
+    copy stream), sized by chunk_rows; one sample per copy span."""
+    from .sliced import CallSpec, NativeLayer, forward_calls
+
+    h = 2 * max(chunk_rows)
+    g = torch.Generator().manual_seed(3)
+    w1t = torch.randn(h, model_dim, generator=g).to(torch.bfloat16)
+    w2 = torch.randn(h, model_dim, generator=g).to(torch.bfloat16)
+    x = torch.randn(1, model_dim, device="cuda").to(torch.bfloat16)
     out = []
-    stream = torch.cuda.current_stream()
-    for n in sizes:
-        src = torch.empty(n, dtype=torch.uint8).pin_memory()
-        dst = torch.empty(n, dtype=torch.uint8, device="cuda")
-        for r in range(reps + 2):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            dst.copy_(src, non_blocking=True)
-            b.record(stream)
-            b.synchronize()
-            if r >= 2:
-                out.append(ProfileSample(OpClass.C2G, float(n), a.elapsed_time(b) * 1e-3))
+    for cr in chunk_rows:
+        lay = NativeLayer(w1t, w2, 0, h, "silu", w1t, dtype="bf16", chunk_rows=cr)
+        for r in range(reps + 1):
+            torch.cuda.synchronize()
+            nat.trace_enable(True)
+            forward_calls([CallSpec(lay)], x)
+            spans = [s for s in nat.trace_fetch() if s["kind"] == "copy"]
+            nat.trace_enable(False)
+            if r >= 1:
+                out += [ProfileSample(OpClass.C2G, float(s["bytes"]), s["end_s"] - s["start_s"]) for s in spans]
+        lay.release()
     return out
 
 
@@ -127,7 +136,7 @@ def launch_samples(torch, reps=20):
     from .sliced import CallSpec, NativeLayer, forward_calls
 
     rng = np.random.default_rng(1)
-    lay = NativeLayer(rng.standard_normal((256, 512), dtype=np.float32), rng.standard_normal((512, 256), dtype=np.float32),
+    lay = NativeLayer(rng.standard_normal((256, 512), dtype=np.float32), rng.standard_normal((256, 512), dtype=np.float32),
                       0, 0, "silu", rng.standard_normal((256, 512), dtype=np.float32), dtype="bf16")
     x = torch.randn(1, 512, device="cuda").to(torch.bfloat16)
     out = []
@@ -156,7 +165,7 @@ def measure(phase: str = "decode", quick: bool = False) -> list[ProfileSample]:
         widths, cpu_widths = [1024, 4096, 14336], [256, 1024, 2048]
     samples = gpu_gemm_samples(torch, tokens, widths, reps=3 if quick else 5)
     samples += cpu_gemm_samples(min(tokens, 8), cpu_widths, reps=2 if quick else 4)
-    samples += c2g_samples(torch, [1 << 16, 1 << 20, 4 << 20, 8 << 20, 16 << 20, 64 << 20])
+    samples += c2g_samples(torch)
     samples += launch_samples(torch)
     return samples
 

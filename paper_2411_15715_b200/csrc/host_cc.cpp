@@ -168,71 +168,111 @@ static inline float act_host(int act, float z) {
 
 static inline int64_t round16(int64_t v) { return (v + 15) / 16 * 16; }
 
+// y[t, 0:n16) += sum_r a[r][t] * W2[r][0:n16) for NR rows at once (ybuf is [T, ldy])
+template <int WD, int NR>
+__attribute__((target("avx512f,avx512bw,fma"))) static void axpy_rows_avx512(
+    const void* const* rows, const float* a /*[NR][T]*/, int64_t T, float* ybuf, int64_t ldy, int64_t n16) {
+  for (int64_t n = 0; n < n16; n += 16) {
+    __m512 w[NR];
+    for (int r = 0; r < NR; ++r) w[r] = load16<WD>(rows[r], n);
+    for (int64_t t = 0; t < T; ++t) {
+      float* yp = ybuf + t * ldy + n;
+      __m512 acc = _mm512_loadu_ps(yp);
+      for (int r = 0; r < NR; ++r) acc = _mm512_fmadd_ps(w[r], _mm512_set1_ps(a[r * T + t]), acc);
+      _mm512_storeu_ps(yp, acc);
+    }
+  }
+}
+
+static void axpy_rows_scalar(const void* const* rows, int nr, const float* a, int64_t T, float* ybuf,
+                             int64_t ldy, int64_t n16, int wd) {
+  for (int r = 0; r < nr; ++r)
+    for (int64_t t = 0; t < T; ++t) {
+      const float at = a[r * T + t];
+      for (int64_t n = 0; n < n16; ++n) ybuf[t * ldy + n] += at * to_f(rows[r], n, wd);
+    }
+}
+
+static void axpy_rows(const void* const* rows, int nr, const float* a, int64_t T, float* ybuf,
+                      int64_t ldy, int64_t n16, int wd) {
+  if (!host_has_avx512()) return axpy_rows_scalar(rows, nr, a, T, ybuf, ldy, n16, wd);
+  while (nr > 0) {
+    const int take = nr >= 4 ? 4 : nr >= 2 ? 2 : 1;
+    if (wd == 1) {
+      if (take == 4) axpy_rows_avx512<1, 4>(rows, a, T, ybuf, ldy, n16);
+      else if (take == 2) axpy_rows_avx512<1, 2>(rows, a, T, ybuf, ldy, n16);
+      else axpy_rows_avx512<1, 1>(rows, a, T, ybuf, ldy, n16);
+    } else {
+      if (take == 4) axpy_rows_avx512<0, 4>(rows, a, T, ybuf, ldy, n16);
+      else if (take == 2) axpy_rows_avx512<0, 2>(rows, a, T, ybuf, ldy, n16);
+      else axpy_rows_avx512<0, 1>(rows, a, T, ybuf, ldy, n16);
+    }
+    rows += take;
+    a += take * T;
+    nr -= take;
+  }
+}
+
 // ---------------------------------------------------------------------------
 
 void cc_forward(const CCProblem& p, ThreadPool& pool, int threads) {
-  if (p.b1 <= 0 || p.T <= 0) {
-    for (int64_t i = 0; i < p.T * p.N; ++i) p.y[i] = 0.f;
+  const int64_t T = p.T;
+  if (p.b1 <= 0 || T <= 0) {
+    for (int64_t i = 0; i < T * p.N; ++i) p.y[i] = 0.f;
     return;
   }
   const int wd = p.wdtype;
   const size_t esz = wd == 1 ? 2 : 4;
-  const int64_t T = p.T;
   const int64_t k_up = round16(p.M);
+  const int64_t n16 = round16(p.N);  // W2 rows are zero padded to ldn >= roundup(N, 64)
+  const int n_thr = int(std::max<int64_t>(1, std::min<int64_t>(std::min(threads, pool.size()), p.b1)));
 
-  // hidden row -> (chunk, local row)
+  // hidden row -> chunk
   std::vector<int> chunk_of(size_t(p.b1));
   for (int c = 0; c < p.n_chunks; ++c)
     for (int64_t r = 0; r < p.chunks[c].rc; ++r) chunk_of[size_t(p.chunks[c].r0 + r)] = c;
 
-  // phase 1: a[t, h] for h in [0, b1), rows split over threads
-  auto up = [&](int tid, int n) {
+  // per-thread partial outputs [n_thr][T][n16]
+  std::vector<float> ybufs(size_t(n_thr) * T * n16, 0.f);
+
+  auto rows_pass = [&](int tid, int n) {
     const int64_t h0 = p.b1 * tid / n, h1 = p.b1 * (tid + 1) / n;
-    std::vector<float> s(size_t(2 * T));
+    float* ybuf = ybufs.data() + size_t(tid) * T * n16;
+    std::vector<float> s(size_t(2 * T)), a(size_t(4 * T));
+    const void* w2rows[4];
+    int pend = 0;
     for (int64_t h = h0; h < h1; ++h) {
       const HostChunk& c = p.chunks[chunk_of[size_t(h)]];
-      const int64_t off = (h - c.r0) * p.ldm * int64_t(esz);
-      const void* rows[2] = {static_cast<const char*>(c.w1t) + off,
-                             p.gated ? static_cast<const char*>(c.w3t) + off : nullptr};
+      const int64_t off1 = (h - c.r0) * p.ldm * int64_t(esz);
+      const void* rows[2] = {static_cast<const char*>(c.w1t) + off1,
+                             p.gated ? static_cast<const char*>(c.w3t) + off1 : nullptr};
       if (p.gated) {
         dot_rows<2>(rows, k_up, p.x, p.ldx, T, wd, s.data());
-        for (int64_t t = 0; t < T; ++t) p.a[t * p.lda + h] = act_host(p.act, s[t]) * s[T + t];
+        for (int64_t t = 0; t < T; ++t) a[pend * T + t] = act_host(p.act, s[t]) * s[T + t];
       } else {
         dot_rows<1>(rows, k_up, p.x, p.ldx, T, wd, s.data());
-        for (int64_t t = 0; t < T; ++t) p.a[t * p.lda + h] = act_host(p.act, s[t]);
+        for (int64_t t = 0; t < T; ++t) a[pend * T + t] = act_host(p.act, s[t]);
+      }
+      w2rows[pend++] = static_cast<const char*>(c.w2) + (h - c.r0) * p.ldn * int64_t(esz);
+      if (pend == 4 || h + 1 == h1) {
+        axpy_rows(w2rows, pend, a.data(), T, ybuf, n16, n16, wd);
+        pend = 0;
       }
     }
   };
-  pool.run(threads, up);
+  pool.run(n_thr, rows_pass);
 
-  // phase 2: y[t, n] over chunks, outputs split over threads
-  auto down = [&](int tid, int n) {
-    const int64_t n0 = p.N * tid / n, n1 = p.N * (tid + 1) / n;
-    std::vector<float> s(size_t(2 * T));
-    for (int64_t o = n0; o < n1; o += 2) {
-      const int pair = (o + 1 < n1) ? 2 : 1;
-      for (int64_t t = 0; t < T; ++t) {
-        p.y[t * p.N + o] = 0.f;
-        if (pair == 2) p.y[t * p.N + o + 1] = 0.f;
+  auto reduce = [&](int tid, int n) {
+    const int64_t c0 = (n16 / 16) * tid / n * 16, c1 = (n16 / 16) * (tid + 1) / n * 16;
+    for (int64_t t = 0; t < T; ++t)
+      for (int64_t col = c0; col < c1; ++col) {
+        if (col >= p.N) break;
+        float v = 0.f;
+        for (int i = 0; i < n_thr; ++i) v += ybufs[(size_t(i) * T + t) * n16 + col];
+        p.y[t * p.N + col] = v;
       }
-      for (int ci = 0; ci < p.n_chunks; ++ci) {
-        const HostChunk& c = p.chunks[ci];
-        const char* base = static_cast<const char*>(c.w2t);
-        const void* rows[2] = {base + o * c.ldc * int64_t(esz),
-                               base + (o + pair - 1) * c.ldc * int64_t(esz)};
-        const int64_t k16 = round16(c.rc);
-        if (pair == 2)
-          dot_rows<2>(rows, k16, p.a + c.r0, p.lda, T, wd, s.data());
-        else
-          dot_rows<1>(rows, k16, p.a + c.r0, p.lda, T, wd, s.data());
-        for (int64_t t = 0; t < T; ++t) {
-          p.y[t * p.N + o] += s[t];
-          if (pair == 2) p.y[t * p.N + o + 1] += s[T + t];
-        }
-      }
-    }
   };
-  pool.run(threads, down);
+  pool.run(threads, reduce);
 }
 
 }  // namespace sp

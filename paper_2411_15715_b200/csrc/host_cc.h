@@ -1,11 +1,13 @@
 // host_cc.h -- the CC block on host cores (Stream-A of PAPER.md:161).
 //
 // The reference computes every block with numpy fp64 on one thread
-// (slicing_kernel.py:119-123).  Here the CC block (hidden columns [0, b1)) is
+// (slicing_kernel.py:119-123).  Here the CC block (hidden units [0, b1)) is
 // computed natively from the same pinned, chunk-interleaved layout the GPU
-// streams from, on a persistent pool of host threads, in fp32 with AVX-512:
-//   a[t, h]  = act(<W1t[h], x[t]>) [* <W3t[h], x[t]>]      rows split over threads
-//   y[t, n]  = sum_chunks <W2t_chunk[n, :rc], a[t, r0:r0+rc]>  outputs split over threads
+// streams from, on a persistent pool of host threads, in fp32 with AVX-512.
+// Thread i owns a contiguous range of hidden units and streams their rows once:
+//   a[t, h]     = act(<W1t[h], x[t]>) [* <W3t[h], x[t]>]
+//   y_i[t, :]  += a[t, h] * W2[h, :]
+// then y = sum_i y_i in thread order (deterministic), split over columns.
 #pragma once
 
 #include <stdint.h>
@@ -43,22 +45,20 @@ class ThreadPool {
 struct HostChunk {
   const void* w1t;  // [rc, ldm]
   const void* w3t;  // [rc, ldm] or null
-  const void* w2t;  // [N, ldc]
-  int64_t r0, rc, ldc;
+  const void* w2;   // [rc, ldn]
+  int64_t r0, rc;
 };
 
 struct CCProblem {
   int wdtype;      // 0 f32, 1 bf16
   int gated, act;
-  int64_t M, N, ldm;
+  int64_t M, N, ldm, ldn;
   const HostChunk* chunks;
   int n_chunks;    // covering hidden rows [0, b1)
   int64_t b1;
   const float* x;  // [T, ldx] fp32, zero padded to ldx >= roundup(M, 64)
   int64_t ldx;
   int64_t T;
-  float* a;        // scratch [T, lda], lda >= roundup(b1, 64), zero padded
-  int64_t lda;
   float* y;        // [T, N] output
 };
 

@@ -1,24 +1,31 @@
 // kernels.cuh -- sm_100a kernels of the sliced FFN path.
 //
-// Every GPU-side product of the path is a "row dot": out[t, r] = epi(<W[r, :K], x[t, :K]>)
-// with W stored row-major, rows padded to a multiple of 64 elements (zero
-// padding), so each hidden column of the reference's W1 / W3 (slicing_kernel.py:
-// 75-76, columns) and each output column of W2 restricted to a row block
-// (slicing_kernel.py:77, rows) is one contiguous, 128-byte aligned row.  The same
-// kernel serves
-//   * the up-projection  a[t, h] = act(<W1t[h], x[t]>) [* <W3t[h], x[t]>]   (K = M)
-//   * the down-projection y[t, n] (+)= <W2t[n, block], a[t, block]>          (K = |block|)
-// for the GG block (weights resident in HBM) and for every streamed CG chunk
-// (weights in the staging ring).  The activation of the reference
-// (slicing_kernel.py:33-38) is fused into the up-projection epilogue.
+// A "block" is a contiguous range of hidden units [h0, h0 + rows) of one FFN
+// instance: the GG block (HBM resident) or one streamed CG chunk (in the HBM
+// staging ring).  Its weights are packed as
+//     W1t[rows, ldm] | W3t[rows, ldm] (gated only) | W2[rows, ldn]
+// i.e. hidden unit h owns row h of each matrix: column h of the reference's
+// W1 / W3 (slicing_kernel.py:75-76) and row h of its W2 (:77); rows are zero
+// padded to a multiple of 64 elements (128-byte aligned).
 //
-// Decode GEMV design (HBM-bound, ~1 flop per weight byte):
-//   * persistent grid: #SMs x resident CTAs, contiguous row ranges per CTA;
-//   * x (the T activations) staged once per CTA in shared memory as fp32;
-//   * 128-bit streaming loads (ld.global.nc.L1::no_allocate) of the weights;
-//   * split-K across WPR warps of a CTA for long rows + warp-shuffle
-//     reductions, a double-buffered smem combine across the WPR warps;
-//   * fp32 accumulation throughout.
+// ffn_block_kernel computes, for every token t of the launch,
+//     a[t, h]   = act(<W1t[h], x[t]>) [* <W3t[h], x[t]>]            (phase 1)
+//     y_c[t, :] = sum_{h in CTA c's rows} a[t, h] * W2[h, :]          (phase 2)
+// and writes y_c -- CTA c's partial of the block's output -- to its own slice
+// of a partial buffer.  reduce_slices_kernel sums the slices of every block of
+// a call in a fixed order (deterministic), merge_kernel adds the CC partial,
+// applies the MoE gates and casts.  The up/down dependency therefore never
+// leaves the CTA: one launch per block, no grid-wide barrier, no `a` round trip.
+//
+// Decode is HBM-bound (~1 flop per weight byte).  Each CTA's rows are
+// contiguous in memory, so one producer lane streams them with cp.async.bulk
+// (TMA bulk-copy engine) through an NST-deep shared-memory ring with
+// full/empty mbarriers; 8 consumer warps read weights only from shared memory:
+//   phase 1: warp w owns k-slice w of every row (x slice staged once), warp
+//            shuffles reduce each (row, matrix), partials parked in smem,
+//            one named barrier combines the 8 slices + fused SiLU/GELU/gate;
+//   phase 2: thread owns 8-element column vectors of W2 rows, FMAs a[t, h]
+//            (smem broadcast) into fp32 registers.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -27,13 +34,11 @@
 
 namespace sp {
 
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
-constexpr int kRowGroup = 2;        // rows a warp works on together (ILP)
-constexpr int kPadElems = 64;       // row padding of every packed matrix
-constexpr int kMaxTileFloats = 16384;  // x tile: TT * KT floats <= 64 KB
-
-enum Mode : int { kUp = 0, kUpGated = 1, kDown = 2 };
+constexpr int kPadElems = 64;          // row padding of every packed matrix
+constexpr int kConsumers = 8;          // consumer warps per CTA
+constexpr int kBlockThreads = (kConsumers + 1) * 32;
+constexpr int kMaxStages = 8;
+constexpr int kMaxVec = 4;             // W2 column vectors per thread (N <= 8192 bf16)
 
 template <typename WT>
 struct VecTraits;
@@ -46,15 +51,7 @@ struct VecTraits<__nv_bfloat16> {
   static constexpr int kElems = 8;
 };
 
-__device__ __forceinline__ uint4 ld_stream(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-// 16 weight bytes -> fp32 lanes
+// 16 weight bytes -> fp32
 template <typename WT>
 __device__ __forceinline__ void unpack(const uint4& u, float* f);
 template <>
@@ -88,117 +85,193 @@ __device__ __forceinline__ int xs_pos(int k, int kt) {
   }
 }
 
+// The reference's activations (slicing_kernel.py:33-38) in fp32.
 __device__ __forceinline__ float act_fn(int act, float z) {
-  if (act == 1) return z / (1.0f + expf(-z));                       // SiLU
+  if (act == 1) return z / (1.0f + expf(-z));                                // SiLU
   if (act == 2) return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f));  // GELU (erf)
   return z;
 }
 
 __device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
 
-struct RowDotArgs {
-  const void* w0;      // rows [0, rows) of length ldw elements
-  const void* w1;      // second matrix (gated up-projection) or nullptr
-  int64_t ldw;         // row stride (elements), multiple of kPadElems
-  int rows;
-  int K;               // valid reduction length <= ldw
-  // activations: x_row(t) = src + (ids ? ids[t0 + t] : t0 + t) * ldx + xcol0
+// ---- mbarrier / bulk-copy primitives ---------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "SP_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra SP_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
+}
+
+struct FfnArgs {
+  const void* w1t;     // [rows, ldm]
+  const void* w3t;     // [rows, ldm] or null
+  const void* w2;      // [rows, ldn]
+  int64_t ldm, ldn;    // row strides (elements)
+  int rows;            // hidden units in the block
+  int M, N;
+  // x row of token t: x + (ids ? ids[t0 + t] : t0 + t) * ldx
   const void* x;
   int xdtype;          // 0 f32, 1 bf16
   int64_t ldx;
-  int64_t xcol0;
-  const int32_t* ids;  // device, may be null
-  int t0;              // first token (row of the call) this launch covers
-  int T;               // tokens this launch covers (<= TT)
-  // output: out[(t0 + t) * ldo + ocol0 + r]
-  float* out;
-  int64_t ldo;
-  int64_t ocol0;
-  int accumulate;      // kDown: add into out instead of overwrite
+  const int32_t* ids;  // device or null
+  int t0, T;           // tokens [t0, t0 + T) of the call (T <= TT)
   int act;
-  int kt;              // x tile length (multiple of 256, <= kMaxTileFloats / TT)
+  int kt;              // x tile: roundup(M, 256)
+  // partial slices: part[(slice0 + blockIdx.x) * slice_stride + (t0 + t) * N + n]
+  float* part;
+  int64_t slice0, slice_stride;
 };
 
-// Shared memory: xs[TT][kt] | red[2][kWarps][kRowGroup*G][TT] | acc[rows_per_cta][G][TT]
-template <typename WT, int TT, int MODE, int WPR>
-__global__ void __launch_bounds__(kThreads) rowdot_kernel(RowDotArgs p) {
+struct FfnPlan {
+  int rs_up;        // hidden rows per phase-1 stage
+  int rs_down;      // hidden rows per phase-2 stage
+  int stages;       // ring depth NST
+  int stage_bytes;  // bytes per ring slot
+};
+
+// smem: ring[NST][stage] | xs[TT][kt] | part1[n_local][8][G][TT] | a_loc[n_local][TT] | bars
+template <typename WT, int TT, bool GATED, int NV>
+__global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, FfnPlan fp) {
   constexpr int VE = VecTraits<WT>::kElems;
-  constexpr int G = (MODE == kUpGated) ? 2 : 1;
-  constexpr int SUBROWS = kWarps / WPR;         // rows processed concurrently by the CTA
-  constexpr int GROUP = SUBROWS * kRowGroup;    // rows per group step
-  extern __shared__ __align__(16) float smem[];
-  float* xs = smem;
-  float* red = xs + TT * p.kt;
-  float* acc = red + 2 * kWarps * kRowGroup * G * TT;
+  constexpr int G = GATED ? 2 : 1;
+  constexpr int STEP = 32 * VE;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sub = warp / WPR, part = warp % WPR;
   const int64_t r_begin = (int64_t)p.rows * blockIdx.x / gridDim.x;
   const int64_t r_end = (int64_t)p.rows * (blockIdx.x + 1) / gridDim.x;
   const int n_local = int(r_end - r_begin);
-  if (n_local <= 0) return;
-  for (int i = threadIdx.x; i < n_local * G * TT; i += kThreads) acc[i] = 0.f;
+  const int NST = fp.stages;
+  const int n_up = (n_local + fp.rs_up - 1) / fp.rs_up;
+  const int n_dn = (n_local + fp.rs_down - 1) / fp.rs_down;
+  const int64_t row1 = p.ldm * int64_t(sizeof(WT)), row2 = p.ldn * int64_t(sizeof(WT));
 
-  const char* wbase[G];
-  wbase[0] = static_cast<const char*>(p.w0);
-  if constexpr (G == 2) wbase[1] = static_cast<const char*>(p.w1);
-  int red_buf = 0;
+  unsigned char* ring = smem_raw;
+  float* xs = reinterpret_cast<float*>(ring + size_t(NST) * fp.stage_bytes);
+  float* part1 = xs + TT * p.kt;
+  float* a_loc = part1 + n_local * kConsumers * G * TT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(a_loc + ((n_local * TT + 1) & ~1));
+  uint64_t* empty = full + NST;
 
-  for (int k0 = 0; k0 < p.K; k0 += p.kt) {
-    const int kt_valid = min(p.kt, p.K - k0);
-    __syncthreads();
-    // ---- stage x[:, k0 : k0 + kt] as fp32 (zero beyond K and beyond T) ----
-    for (int i = threadIdx.x; i < TT * p.kt; i += kThreads) {
-      const int t = i / p.kt, k = i - t * p.kt;
-      float v = 0.f;
-      if (t < p.T && k < kt_valid) {
-        const int64_t row = p.ids ? p.ids[p.t0 + t] : int64_t(p.t0 + t);
-        const int64_t off = row * p.ldx + p.xcol0 + k0 + k;
-        v = p.xdtype == 1 ? bf16_to_f(static_cast<const uint16_t*>(p.x)[off])
-                          : static_cast<const float*>(p.x)[off];
-      }
-      xs[t * p.kt + xs_pos<WT>(k, p.kt)] = v;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
     }
-    __syncthreads();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
 
-    // this warp's k-slice of the tile, rounded to whole vectors
-    const int per_part = ((kt_valid + WPR - 1) / WPR + VE - 1) / VE * VE;
-    const int kb = part * per_part;
-    const int ke = min(kt_valid, kb + per_part);
+  if (warp == kConsumers) {
+    // ---------------- producer: one lane streams the CTA's rows ----------------
+    if (lane == 0 && n_local > 0) {
+      const uint64_t pol = evict_first_policy();
+      const char* s1 = static_cast<const char*>(p.w1t) + r_begin * row1;
+      const char* s3 = GATED ? static_cast<const char*>(p.w3t) + r_begin * row1 : nullptr;
+      const char* s2 = static_cast<const char*>(p.w2) + r_begin * row2;
+      for (int s = 0; s < n_up + n_dn; ++s) {
+        const int slot = s % NST;
+        if (s >= NST) mbar_wait(&empty[slot], ((s / NST) - 1) & 1);
+        unsigned char* dst = ring + size_t(slot) * fp.stage_bytes;
+        if (s < n_up) {
+          const int rows_s = min(fp.rs_up, n_local - s * fp.rs_up);
+          const uint32_t bytes = uint32_t(rows_s * row1);
+          mbar_expect_tx(&full[slot], bytes * G);
+          bulk_g2s(dst, s1 + int64_t(s) * fp.rs_up * row1, bytes, &full[slot], pol);
+          if constexpr (GATED)
+            bulk_g2s(dst + size_t(fp.rs_up) * row1, s3 + int64_t(s) * fp.rs_up * row1, bytes, &full[slot], pol);
+        } else {
+          const int d = s - n_up;
+          const int rows_s = min(fp.rs_down, n_local - d * fp.rs_down);
+          const uint32_t bytes = uint32_t(rows_s * row2);
+          mbar_expect_tx(&full[slot], bytes);
+          bulk_g2s(dst, s2 + int64_t(d) * fp.rs_down * row2, bytes, &full[slot], pol);
+        }
+      }
+    }
+    return;
+  }
 
-    for (int g0 = 0; g0 < n_local; g0 += GROUP) {
-      float s[kRowGroup][G][TT];
+  // ---------------- consumers ----------------
+  // stage x[:, 0:M) as fp32 (overlaps the first bulk copies); zero beyond M / T
+  for (int t = 0; t < TT; ++t) {
+    const bool live_t = t < p.T;
+    const int64_t row = live_t ? (p.ids ? p.ids[p.t0 + t] : int64_t(p.t0 + t)) : 0;
+    const int64_t base = row * p.ldx;
+    float* xrow = xs + t * p.kt;
+    for (int k = threadIdx.x; k < p.kt; k += kConsumers * 32) {
+      float v = 0.f;
+      if (live_t && k < p.M)
+        v = p.xdtype == 1 ? bf16_to_f(static_cast<const uint16_t*>(p.x)[base + k])
+                          : static_cast<const float*>(p.x)[base + k];
+      xrow[xs_pos<WT>(k, p.kt)] = v;
+    }
+  }
+  consumers_sync();
+
+  // ---- phase 1: a[t, h] for the CTA's rows ----
+  // vectors [k, k + VE) with k < M stay inside the zero-padded row and meet zero x beyond M
+  const int steps_total = (p.M + STEP - 1) / STEP;
+  const int per = (steps_total + kConsumers - 1) / kConsumers;
+  const int kb = warp * per * STEP;
+  const int ke = min((p.M + VE - 1) / VE * VE, kb + per * STEP);
+  for (int s = 0; s < n_up; ++s) {
+    const int slot = s % NST;
+    mbar_wait(&full[slot], (s / NST) & 1);
+    const int rows_s = min(fp.rs_up, n_local - s * fp.rs_up);
+    const unsigned char* st = ring + size_t(slot) * fp.stage_bytes;
+    for (int j = 0; j < rows_s; ++j) {
+      float acc[G][TT];
 #pragma unroll
-      for (int j = 0; j < kRowGroup; ++j)
+      for (int m = 0; m < G; ++m)
+#pragma unroll
+        for (int t = 0; t < TT; ++t) acc[m][t] = 0.f;
+#pragma unroll 4
+      for (int k = kb + lane * VE; k < ke; k += STEP) {
+        uint4 wv[G];
 #pragma unroll
         for (int m = 0; m < G; ++m)
-#pragma unroll
-          for (int t = 0; t < TT; ++t) s[j][m][t] = 0.f;
-
-      int64_t rows_j[kRowGroup];
-      bool live[kRowGroup];
-#pragma unroll
-      for (int j = 0; j < kRowGroup; ++j) {
-        const int lr = g0 + sub * kRowGroup + j;
-        live[j] = lr < n_local;
-        rows_j[j] = r_begin + (live[j] ? lr : 0);
-      }
-
-#pragma unroll 2
-      for (int k = kb + lane * VE; k < ke; k += 32 * VE) {
-        uint4 wv[kRowGroup][G];
-#pragma unroll
-        for (int j = 0; j < kRowGroup; ++j)
-#pragma unroll
-          for (int m = 0; m < G; ++m) {
-            const char* ptr = wbase[m] + (rows_j[j] * p.ldw + k0 + k) * sizeof(WT);
-            wv[j][m] = live[j] ? ld_stream(ptr) : make_uint4(0, 0, 0, 0);
-          }
+          wv[m] = *reinterpret_cast<const uint4*>(st + (size_t(m) * fp.rs_up + j) * row1 + size_t(k) * sizeof(WT));
+        const int pos = xs_pos<WT>(k, p.kt);
 #pragma unroll
         for (int t = 0; t < TT; ++t) {
           float xv[VE];
           const float* xrow = xs + t * p.kt;
-          const int pos = xs_pos<WT>(k, p.kt);
           const float4 a = *reinterpret_cast<const float4*>(xrow + pos);
           xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
           if constexpr (VE == 8) {
@@ -206,86 +279,146 @@ __global__ void __launch_bounds__(kThreads) rowdot_kernel(RowDotArgs p) {
             xv[4] = b.x; xv[5] = b.y; xv[6] = b.z; xv[7] = b.w;
           }
 #pragma unroll
-          for (int j = 0; j < kRowGroup; ++j)
+          for (int m = 0; m < G; ++m) {
+            float wf[VE];
+            unpack<WT>(wv[m], wf);
 #pragma unroll
-            for (int m = 0; m < G; ++m) {
-              float wf[VE];
-              unpack<WT>(wv[j][m], wf);
-#pragma unroll
-              for (int e = 0; e < VE; ++e) s[j][m][t] = fmaf(wf[e], xv[e], s[j][m][t]);
-            }
+            for (int e = 0; e < VE; ++e) acc[m][t] = fmaf(wf[e], xv[e], acc[m][t]);
+          }
         }
       }
-      // warp reduction
 #pragma unroll
-      for (int j = 0; j < kRowGroup; ++j)
+      for (int m = 0; m < G; ++m)
 #pragma unroll
-        for (int m = 0; m < G; ++m)
+        for (int t = 0; t < TT; ++t) {
+          float v = acc[m][t];
 #pragma unroll
-          for (int t = 0; t < TT; ++t) {
-            float v = s[j][m][t];
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-            s[j][m][t] = v;
-          }
-      if constexpr (WPR == 1) {
-        if (lane == 0) {
-#pragma unroll
-          for (int j = 0; j < kRowGroup; ++j)
-            if (live[j]) {
-              const int lr = g0 + sub * kRowGroup + j;
-#pragma unroll
-              for (int m = 0; m < G; ++m)
-#pragma unroll
-                for (int t = 0; t < TT; ++t) acc[(lr * G + m) * TT + t] += s[j][m][t];
-            }
+          for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+          if (lane == 0) part1[(((s * fp.rs_up + j) * kConsumers + warp) * G + m) * TT + t] = v;
         }
-      } else {
-        float* rb = red + red_buf * (kWarps * kRowGroup * G * TT);
-        if (lane == 0) {
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+  consumers_sync();
+  for (int i = threadIdx.x; i < n_local * TT; i += kConsumers * 32) {
+    const int lr = i / TT, t = i - lr * TT;
+    float v[G];
 #pragma unroll
-          for (int j = 0; j < kRowGroup; ++j)
+    for (int m = 0; m < G; ++m) {
+      v[m] = 0.f;
 #pragma unroll
-            for (int m = 0; m < G; ++m)
+      for (int q = 0; q < kConsumers; ++q) v[m] += part1[((lr * kConsumers + q) * G + m) * TT + t];
+    }
+    float a = act_fn(p.act, v[0]);
+    if constexpr (GATED) a *= v[1];
+    a_loc[lr * TT + t] = t < p.T ? a : 0.f;
+  }
+  consumers_sync();
+
+  // ---- phase 2: y_c[t, :] = sum_h a[t, h] * W2[h, :] ----
+  const int tid = threadIdx.x;
+  const int n_vec = (p.N + VE - 1) / VE;
+  float acc2[NV][VE][TT];
 #pragma unroll
-              for (int t = 0; t < TT; ++t) rb[((warp * kRowGroup + j) * G + m) * TT + t] = s[j][m][t];
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int e = 0; e < VE; ++e)
+#pragma unroll
+      for (int t = 0; t < TT; ++t) acc2[v][e][t] = 0.f;
+  for (int d = 0; d < n_dn; ++d) {
+    const int s = n_up + d;
+    const int slot = s % NST;
+    mbar_wait(&full[slot], (s / NST) & 1);
+    const int rows_s = min(fp.rs_down, n_local - d * fp.rs_down);
+    const unsigned char* st = ring + size_t(slot) * fp.stage_bytes;
+    for (int j = 0; j < rows_s; ++j) {
+      const int lr = d * fp.rs_down + j;
+      float at[TT];
+#pragma unroll
+      for (int t = 0; t < TT; ++t) at[t] = a_loc[lr * TT + t];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int vec = tid + v * kConsumers * 32;
+        if (vec < n_vec) {
+          const uint4 w = *reinterpret_cast<const uint4*>(st + size_t(j) * row2 + size_t(vec) * 16);
+          float wf[VE];
+          unpack<WT>(w, wf);
+#pragma unroll
+          for (int e = 0; e < VE; ++e)
+#pragma unroll
+            for (int t = 0; t < TT; ++t) acc2[v][e][t] = fmaf(wf[e], at[t], acc2[v][e][t]);
         }
-        __syncthreads();
-        // combine the WPR partial sums of every (row, matrix, token)
-        for (int i = threadIdx.x; i < SUBROWS * kRowGroup * G * TT; i += kThreads) {
-          const int t = i % TT, m = (i / TT) % G, j = (i / (TT * G)) % kRowGroup,
-                    sr = i / (TT * G * kRowGroup);
-          const int lr = g0 + sr * kRowGroup + j;
-          if (lr < n_local) {
-            float v = 0.f;
-#pragma unroll
-            for (int q = 0; q < WPR; ++q) v += rb[(((sr * WPR + q) * kRowGroup + j) * G + m) * TT + t];
-            acc[(lr * G + m) * TT + t] += v;
-          }
-        }
-        red_buf ^= 1;
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
   }
-  __syncthreads();
-  // ---- epilogue ----
-  for (int i = threadIdx.x; i < n_local * TT; i += kThreads) {
-    const int lr = i / TT, t = i - lr * TT;
-    if (t >= p.T) continue;
-    float* o = p.out + int64_t(p.t0 + t) * p.ldo + p.ocol0 + r_begin + lr;
-    if constexpr (MODE == kDown) {
-      const float v = acc[lr * TT + t];
-      *o = p.accumulate ? *o + v : v;
-    } else if constexpr (MODE == kUp) {
-      *o = act_fn(p.act, acc[lr * TT + t]);
-    } else {
-      *o = act_fn(p.act, acc[(lr * 2 + 0) * TT + t]) * acc[(lr * 2 + 1) * TT + t];
+  // write this CTA's partial slice (a CTA with no rows writes zeros)
+  float* out = p.part + (p.slice0 + blockIdx.x) * p.slice_stride;
+#pragma unroll
+  for (int t = 0; t < TT; ++t) {
+    if (t >= p.T) break;
+    float* orow = out + int64_t(p.t0 + t) * p.N;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int vec = tid + v * kConsumers * 32;
+      if (vec >= n_vec) continue;
+      const int n0 = vec * VE;
+      if (n0 + VE <= p.N && (p.N & 3) == 0) {
+#pragma unroll
+        for (int e = 0; e < VE; e += 4)
+          *reinterpret_cast<float4*>(orow + n0 + e) =
+              make_float4(acc2[v][e][t], acc2[v][e + 1][t], acc2[v][e + 2][t], acc2[v][e + 3][t]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VE; ++e)
+          if (n0 + e < p.N) orow[n0 + e] = acc2[v][e][t];
+      }
     }
   }
 }
 
+// ---- slice reduction: y_c[i, n] (+)= sum_s part_c[s, i, n], fixed order -------------
+constexpr int kMaxCalls = 32;
+struct ReduceCall {
+  const float* part;  // [S][T_e][N]
+  float* y;           // [T_e][N]
+  int S, T_e;
+  int accumulate;
+};
+struct ReduceArgs {
+  ReduceCall c[kMaxCalls];
+  int row_start[kMaxCalls + 1];  // prefix sums of T_e
+  int n_calls;
+  int N;
+};
+
+// grid (ceil(N / 32), total rows); block 256 = 32 columns x 8 slice groups
+__global__ void __launch_bounds__(256) reduce_slices_kernel(ReduceArgs p) {
+  __shared__ float red[8][33];
+  const int row = blockIdx.y;
+  int c = 0;
+  while (c + 1 < p.n_calls && row >= p.row_start[c + 1]) ++c;
+  const ReduceCall& rc = p.c[c];
+  const int i = row - p.row_start[c];
+  const int col = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int n = blockIdx.x * 32 + col;
+  float v = 0.f;
+  if (n < p.N)
+    for (int s = grp; s < rc.S; s += 8) v += rc.part[(int64_t(s) * rc.T_e + i) * p.N + n];
+  red[grp][col] = v;
+  __syncthreads();
+  if (grp == 0 && n < p.N) {
+    float tot = 0.f;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) tot += red[g][col];
+    float* o = rc.y + int64_t(i) * p.N + n;
+    *o = rc.accumulate ? *o + tot : tot;
+  }
+}
+
 // ---- merge: y[t] = sum_c sum_{i: ids_c[i]=t} gate_c[i] * (y_gpu_c[i] + y_cc_c[i]) -------
-constexpr int kMaxMergeCalls = 32;
 struct MergeCall {
   const float* y_gpu;    // [T_e, N]
   const float* y_cc;     // [T_e, N] or null; rows >= n_cc are absent
@@ -295,7 +428,7 @@ struct MergeCall {
   int n_cc;
 };
 struct MergeArgs {
-  MergeCall c[kMaxMergeCalls];
+  MergeCall c[kMaxCalls];
   int n_calls;
   int T;
   int64_t N;

@@ -10,6 +10,7 @@
 // and sums the partial outputs in a merge kernel.
 #include <cuda_runtime.h>
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -25,6 +26,7 @@
 #include "../../include/sliced.h"
 #include "host_cc.h"
 #include "kernels.cuh"
+
 
 namespace sp {
 
@@ -146,9 +148,15 @@ static Context* ctx_or_null() { return g_ctx.get(); }
 
 // ---------------------------------------------------------------------------
 // layer placement
+//
+// Packed block layout (see kernels.cuh): W1t[rows, ldm] | W3t[rows, ldm] | W2[rows, ldn].
+// GG block rows [b2, H) live in HBM; CC rows [0, b1) and CG rows [b1, b2) live in
+// one pinned host region as chunks of chunk_rows hidden units, each chunk one
+// contiguous (4 KB aligned) copy.  CC chunks double as the stream for the n_g
+// rows diverted to the GPU (cg_prime).
 
 struct Chunk {
-  int64_t r0, rc, ldc;
+  int64_t r0, rc;
   size_t off, bytes;       // within the pinned host region
   size_t w3_off, w2_off;   // offsets inside the chunk
   bool cc;
@@ -160,9 +168,9 @@ struct sp_layer {
   sp_layer_desc d;
   int device;
   size_t esz;
-  int64_t ldm;             // padded M
+  int64_t ldm, ldn;        // padded M, padded N
   // GG (HBM)
-  int64_t h_gg, ld_gg;
+  int64_t h_gg;
   void* gg = nullptr;
   size_t gg_bytes = 0, gg_w3_off = 0, gg_w2_off = 0;
   // host region (pinned): CC chunks then CG chunks
@@ -176,25 +184,32 @@ struct sp_layer {
 
 namespace sp {
 
-static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void* w2t) {
+// Copy rows [r0, r0 + n) of a row-major [*, cols] source into a [n, ld] block.
+static void copy_rows(char* dst, int64_t ld, const char* src, int64_t cols, int64_t r0, int64_t n,
+                      size_t esz) {
+  for (int64_t r = 0; r < n; ++r)
+    memcpy(dst + size_t(r) * ld * esz, src + size_t(r0 + r) * cols * esz, size_t(cols) * esz);
+}
+
+static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void* w2) {
   const sp_layer_desc& d = L->d;
   const int64_t M = d.model_dim, H = d.hidden_dim, N = d.out_dim;
   const size_t esz = L->esz;
   const char* s1 = static_cast<const char*>(w1t);
   const char* s3 = static_cast<const char*>(w3t);
-  const char* s2 = static_cast<const char*>(w2t);
+  const char* s2 = static_cast<const char*>(w2);
   const int G = d.gated ? 2 : 1;
+  (void)H;
 
-  // ---- GG block -> HBM: [W1t rows b2..H | W3t rows | W2t[:, b2:H]] ----
-  L->h_gg = H - d.b2;
-  L->ld_gg = round_up(std::max<int64_t>(L->h_gg, 1), kPadElems);
+  // ---- GG block -> HBM ----
+  L->h_gg = d.hidden_dim - d.b2;
   if (L->h_gg > 0 && L->host_only)
     return fail(SP_ERR_STATE, "host-only context: a GG block (b2 < H) needs a CUDA device");
   if (L->h_gg > 0) {
     const size_t up = size_t(L->h_gg) * L->ldm * esz;
     L->gg_w3_off = up;
     L->gg_w2_off = up * G;
-    L->gg_bytes = up * G + size_t(N) * L->ld_gg * esz;
+    L->gg_bytes = up * G + size_t(L->h_gg) * L->ldn * esz;
     SP_CUDA(cudaMalloc(&L->gg, L->gg_bytes));
     SP_CUDA(cudaMemset(L->gg, 0, L->gg_bytes));
     char* g = static_cast<char*>(L->gg);
@@ -203,14 +218,14 @@ static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void*
     if (G == 2)
       SP_CUDA(cudaMemcpy2D(g + L->gg_w3_off, L->ldm * esz, s3 + size_t(d.b2) * M * esz, M * esz,
                            M * esz, L->h_gg, cudaMemcpyHostToDevice));
-    SP_CUDA(cudaMemcpy2D(g + L->gg_w2_off, L->ld_gg * esz, s2 + size_t(d.b2) * esz, H * esz,
-                         L->h_gg * esz, N, cudaMemcpyHostToDevice));
+    SP_CUDA(cudaMemcpy2D(g + L->gg_w2_off, L->ldn * esz, s2 + size_t(d.b2) * N * esz, N * esz,
+                         N * esz, L->h_gg, cudaMemcpyHostToDevice));
   }
 
   // ---- CC and CG blocks -> pinned host, chunk-interleaved ----
   int64_t cr = d.chunk_rows;
   if (cr <= 0) {
-    const int64_t row_bytes = (G * L->ldm + N) * int64_t(esz);
+    const int64_t row_bytes = (G * L->ldm + L->ldn) * int64_t(esz);
     cr = std::max<int64_t>(kPadElems, ((int64_t(8) << 20) / row_bytes) / kPadElems * kPadElems);
   }
   cr = round_up(cr, kPadElems);
@@ -221,12 +236,11 @@ static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void*
       Chunk c;
       c.r0 = r0;
       c.rc = std::min(cr, hi - r0);
-      c.ldc = round_up(c.rc, kPadElems);
       c.cc = cc;
       const size_t up = size_t(c.rc) * L->ldm * esz;
       c.w3_off = up;
       c.w2_off = up * G;
-      c.bytes = up * G + size_t(N) * c.ldc * esz;
+      c.bytes = up * G + size_t(c.rc) * L->ldn * esz;
       c.off = off;
       off += round_up(int64_t(c.bytes), 4096);
       L->max_chunk_bytes = std::max(L->max_chunk_bytes, c.bytes);
@@ -243,21 +257,16 @@ static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void*
       L->host = aligned_alloc(4096, off);
       if (!L->host) return fail(SP_ERR_NOMEM, "aligned_alloc(%zu) failed", off);
     } else if (cudaHostAlloc(&L->host, off, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
       return fail(SP_ERR_NOMEM, "cudaHostAlloc(%zu) for the CC/CG blocks failed", off);
     }
     memset(L->host, 0, off);
     char* h = static_cast<char*>(L->host);
     for (const Chunk& c : L->chunks) {
       char* base = h + c.off;
-      for (int64_t r = 0; r < c.rc; ++r) {
-        memcpy(base + size_t(r) * L->ldm * esz, s1 + size_t(c.r0 + r) * M * esz, M * esz);
-        if (G == 2)
-          memcpy(base + c.w3_off + size_t(r) * L->ldm * esz, s3 + size_t(c.r0 + r) * M * esz,
-                 M * esz);
-      }
-      for (int64_t n = 0; n < N; ++n)
-        memcpy(base + c.w2_off + size_t(n) * c.ldc * esz, s2 + (size_t(n) * H + c.r0) * esz,
-               c.rc * esz);
+      copy_rows(base, L->ldm, s1, M, c.r0, c.rc, esz);
+      if (G == 2) copy_rows(base + c.w3_off, L->ldm, s3, M, c.r0, c.rc, esz);
+      copy_rows(base + c.w2_off, L->ldn, s2, N, c.r0, c.rc, esz);
     }
   }
   return SP_OK;
@@ -266,132 +275,134 @@ static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void*
 // ---------------------------------------------------------------------------
 // kernel dispatch
 
-template <typename WT, int TT, int MODE, int WPR>
-static int launch_rowdot_t(Context* C, const RowDotArgs& a, cudaStream_t s) {
-  auto kern = rowdot_kernel<WT, TT, MODE, WPR>;
-  constexpr int G = MODE == kUpGated ? 2 : 1;
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+// Tunables (read once): stage size target, ring depth cap, minimum hidden rows per CTA.
+static const int g_stage_bytes = env_int("SP_STAGE_KB", 32) * 1024;
+static const int g_max_stages = std::min(kMaxStages, env_int("SP_STAGES", kMaxStages));
+static const int g_min_rows_per_cta = std::max(1, env_int("SP_MIN_ROWS", 4));
+constexpr int kSmemLimit = 227 * 1024;
+constexpr int kMaxTileFloats = 16384;  // TT * roundup(M, 256) floats of x <= 64 KB
+
+// CTAs a block of `rows` hidden units is split over (also its partial-slice count).
+static int block_grid(const Context* C, int64_t rows) {
+  if (rows <= 0) return 0;
+  const int64_t by_rows = (rows + g_min_rows_per_cta - 1) / g_min_rows_per_cta;
+  return int(std::max<int64_t>(1, std::min<int64_t>(C->num_sms, by_rows)));
+}
+
+// Largest token tile (1, 2 or 4) whose x copy fits the 64 KB budget.
+static int max_token_tile(int64_t M) {
+  const int64_t kt = round_up(M, 256);
+  for (int tt : {4, 2, 1})
+    if (tt * kt <= kMaxTileFloats) return tt;
+  return 0;
+}
+
+template <typename WT, int TT, bool GATED, int NV>
+static int launch_ffn_t(Context* C, const FfnArgs& a, int grid, cudaStream_t s) {
+  constexpr int G = GATED ? 2 : 1;
+  auto kern = ffn_block_kernel<WT, TT, GATED, NV>;
   static bool attr_set = false;
   if (!attr_set) {
-    SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
     attr_set = true;
   }
-  // first guess of the grid: occupancy at the per-CTA accumulator size for 1 wave
-  const size_t fixed = size_t(TT) * a.kt + 2 * kWarps * kRowGroup * G * TT;
-  auto key = std::make_pair(reinterpret_cast<const void*>(kern), fixed);
-  int occ;
-  auto it = C->occ_cache.find(key);
-  if (it == C->occ_cache.end()) {
-    SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads,
-                                                          (fixed + 64 * G * TT) * sizeof(float)));
-    occ = std::max(1, std::min(occ, 4));
-    C->occ_cache[key] = occ;
-  } else {
-    occ = it->second;
-  }
-  const int grid = std::max(1, std::min(a.rows, C->num_sms * occ));
   const int per_cta = (a.rows + grid - 1) / grid;
-  const size_t smem = (fixed + size_t(per_cta) * G * TT) * sizeof(float);
-  kern<<<grid, kThreads, smem, s>>>(a);
+  const int64_t row1 = a.ldm * int64_t(sizeof(WT)), row2 = a.ldn * int64_t(sizeof(WT));
+  int rs_up = int(std::max<int64_t>(1, g_stage_bytes / (G * row1)));
+  int rs_dn = int(std::max<int64_t>(1, g_stage_bytes / row2));
+  rs_up = std::min(rs_up, per_cta);
+  rs_dn = std::min(rs_dn, per_cta);
+  const size_t stage = size_t(std::max<int64_t>(G * rs_up * row1, rs_dn * row2));
+  const size_t fixed = size_t(TT) * a.kt * 4 + size_t(per_cta) * kConsumers * G * TT * 4 +
+                       size_t((per_cta * TT + 1) & ~1) * 4 + 2 * kMaxStages * 8 + 128;
+  if (fixed + 2 * stage > size_t(kSmemLimit))
+    return fail(SP_ERR_VALUE, "block of %d rows (M=%d, N=%d) does not fit shared memory", a.rows, a.M, a.N);
+  const int nst = int(std::min<size_t>(g_max_stages, (kSmemLimit - fixed) / stage));
+  FfnPlan fp{rs_up, rs_dn, nst, int(stage)};
+  kern<<<grid, kBlockThreads, size_t(nst) * stage + fixed, s>>>(a, fp);
   SP_CUDA(cudaGetLastError());
   ++C->launches;
   return SP_OK;
 }
 
-template <typename WT, int TT, int MODE>
-static int launch_wpr(Context* C, int wpr, const RowDotArgs& a, cudaStream_t s) {
-  switch (wpr) {
-    case 1: return launch_rowdot_t<WT, TT, MODE, 1>(C, a, s);
-    case 4: return launch_rowdot_t<WT, TT, MODE, 4>(C, a, s);
-    default: return launch_rowdot_t<WT, TT, MODE, 8>(C, a, s);
-  }
+template <typename WT, int TT, bool GATED>
+static int launch_nv(Context* C, const FfnArgs& a, int grid, cudaStream_t s) {
+  const int n_vec = (a.N + VecTraits<WT>::kElems - 1) / VecTraits<WT>::kElems;
+  const int nv = (n_vec + kConsumers * 32 - 1) / (kConsumers * 32);
+  if (nv <= 1) return launch_ffn_t<WT, TT, GATED, 1>(C, a, grid, s);
+  if (nv <= 2) return launch_ffn_t<WT, TT, GATED, 2>(C, a, grid, s);
+  if (nv <= 4) return launch_ffn_t<WT, TT, GATED, 4>(C, a, grid, s);
+  return fail(SP_ERR_VALUE, "out_dim %d exceeds the kernel's %d column vectors per thread", a.N, kMaxVec);
 }
 
-template <typename WT, int MODE>
-static int launch_tt(Context* C, int tt, int wpr, const RowDotArgs& a, cudaStream_t s) {
+template <typename WT, bool GATED>
+static int launch_tt(Context* C, int tt, const FfnArgs& a, int grid, cudaStream_t s) {
   switch (tt) {
-    case 1: return launch_wpr<WT, 1, MODE>(C, wpr, a, s);
-    case 2: return launch_wpr<WT, 2, MODE>(C, wpr, a, s);
-    case 4: return launch_wpr<WT, 4, MODE>(C, wpr, a, s);
-    default: return launch_wpr<WT, 8, MODE>(C, wpr, a, s);
+    case 1: return launch_nv<WT, 1, GATED>(C, a, grid, s);
+    case 2: return launch_nv<WT, 2, GATED>(C, a, grid, s);
+    default: return launch_nv<WT, 4, GATED>(C, a, grid, s);
   }
 }
 
-// Launches enough token blocks of <= 8 rows to cover tokens [t0, t0 + T).
-static int rowdot(Context* C, int wdtype, int mode, RowDotArgs a, int t0, int T, cudaStream_t s) {
-  if (a.rows <= 0 || T <= 0) return SP_OK;
-  const int wpr = a.K > 4096 ? 8 : (a.K > 1024 ? 4 : 1);
-  for (int tb = 0; tb < T; tb += 8) {
-    const int n = std::min(8, T - tb);
-    const int tt = n <= 1 ? 1 : n <= 2 ? 2 : n <= 4 ? 4 : 8;
-    a.t0 = t0 + tb;
-    a.T = n;
-    a.kt = int(std::min<int64_t>(round_up(a.K, 256), (kMaxTileFloats / tt) / 256 * 256));
-    int st;
-    if (wdtype == SP_BF16) {
-      st = mode == kUp ? launch_tt<__nv_bfloat16, kUp>(C, tt, wpr, a, s)
-         : mode == kUpGated ? launch_tt<__nv_bfloat16, kUpGated>(C, tt, wpr, a, s)
-                            : launch_tt<__nv_bfloat16, kDown>(C, tt, wpr, a, s);
-    } else {
-      st = mode == kUp ? launch_tt<float, kUp>(C, tt, wpr, a, s)
-         : mode == kUpGated ? launch_tt<float, kUpGated>(C, tt, wpr, a, s)
-                            : launch_tt<float, kDown>(C, tt, wpr, a, s);
-    }
-    SP_TRY(st);
-  }
-  return SP_OK;
-}
-
-// One weight block (GG or a streamed chunk) applied to tokens [t0, t0 + T) of a call:
-//   a[:, col0 : col0 + rows] = act(W1t x) [* W3t x];   y += W2t a[:, col0 : ...]
+// One weight block applied to tokens [t0, t0 + T) of a call: partial slices
+// [slice0, slice0 + grid) of the call's partial buffer.
 struct BlockView {
-  const char* base;    // W1t at base, W3t at base + w3_off, W2t at base + w2_off
+  const char* base;    // W1t at base, W3t at base + w3_off, W2 at base + w2_off
   size_t w3_off, w2_off;
-  int64_t rows, ldm, ldc, col0;
+  int64_t rows;
 };
 
 struct CallWs {
-  float* a;      // [T_e, ldh]
-  float* y;      // [T_e, N]
-  float* ycc;    // [T_e, N]
-  int32_t* ids;  // device
-  float* gates;  // device
-  int64_t ldh;
+  float* part;     // [S][T_e][N] partial slices of every block of the call
+  int S;           // slices in use
+  float* y;        // [T_e, N] reduced GPU partial
+  float* ycc;      // [T_e, N] CC partial (from the host)
+  int32_t* ids;    // device
+  float* gates;    // device
 };
 
 static int run_block(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,
-                     int64_t ldx, const CallWs& w, int t0, int T, bool accumulate, cudaStream_t s) {
-  RowDotArgs up{};
-  up.w0 = b.base;
-  up.w1 = L->d.gated ? b.base + b.w3_off : nullptr;
-  up.ldw = b.ldm;
-  up.rows = int(b.rows);
-  up.K = int(L->d.model_dim);
-  up.x = x;
-  up.xdtype = xdtype;
-  up.ldx = ldx;
-  up.xcol0 = 0;
-  up.ids = w.ids;
-  up.out = w.a;
-  up.ldo = w.ldh;
-  up.ocol0 = b.col0;
-  up.act = L->d.act;
-  SP_TRY(rowdot(C, L->d.wdtype, L->d.gated ? kUpGated : kUp, up, t0, T, s));
-
-  RowDotArgs dn{};
-  dn.w0 = b.base + b.w2_off;
-  dn.ldw = b.ldc;
-  dn.rows = int(L->d.out_dim);
-  dn.K = int(b.rows);
-  dn.x = w.a;
-  dn.xdtype = 0;
-  dn.ldx = w.ldh;
-  dn.xcol0 = b.col0;
-  dn.ids = nullptr;
-  dn.out = w.y;
-  dn.ldo = L->d.out_dim;
-  dn.ocol0 = 0;
-  dn.accumulate = accumulate ? 1 : 0;
-  return rowdot(C, L->d.wdtype, kDown, dn, t0, T, s);
+                     int64_t ldx, CallWs& w, int64_t T_e, int t0, int T, cudaStream_t s) {
+  const int grid = block_grid(C, b.rows);
+  const int tt_max = max_token_tile(L->d.model_dim);
+  if (tt_max == 0) return fail(SP_ERR_VALUE, "model_dim %lld exceeds the x tile", (long long)L->d.model_dim);
+  FfnArgs a{};
+  a.w1t = b.base;
+  a.w3t = L->d.gated ? b.base + b.w3_off : nullptr;
+  a.w2 = b.base + b.w2_off;
+  a.ldm = L->ldm;
+  a.ldn = L->ldn;
+  a.rows = int(b.rows);
+  a.M = int(L->d.model_dim);
+  a.N = int(L->d.out_dim);
+  a.x = x;
+  a.xdtype = xdtype;
+  a.ldx = ldx;
+  a.ids = w.ids;
+  a.act = L->d.act;
+  a.kt = int(round_up(L->d.model_dim, 256));
+  a.part = w.part;
+  a.slice0 = w.S;
+  a.slice_stride = T_e * L->d.out_dim;
+  for (int tb = 0; tb < T; tb += tt_max) {
+    const int n = std::min(tt_max, T - tb);
+    const int tt = n <= 1 ? 1 : n <= 2 ? 2 : 4;
+    a.t0 = t0 + tb;
+    a.T = n;
+    int st;
+    if (L->d.wdtype == SP_BF16)
+      st = L->d.gated ? launch_tt<__nv_bfloat16, true>(C, tt, a, grid, s)
+                      : launch_tt<__nv_bfloat16, false>(C, tt, a, grid, s);
+    else
+      st = L->d.gated ? launch_tt<float, true>(C, tt, a, grid, s) : launch_tt<float, false>(C, tt, a, grid, s);
+    SP_TRY(st);
+  }
+  w.S += grid;
+  return SP_OK;
 }
 
 static double now_s() {
@@ -409,7 +420,7 @@ static cudaEvent_t trace_event(Context* C) {
   return e;
 }
 
-// GPU span bracketing the work enqueued on `s` between begin and end.
+// GPU span bracketing the work enqueued on `s` between construction and end().
 struct GpuSpan {
   Context* C;
   cudaStream_t s;
@@ -446,14 +457,41 @@ static void host_span(Context* C, int stream, int kind, double a, double b, doub
   C->trace.spans.push_back(sp);
 }
 
+static std::vector<HostChunk> host_cc_chunks(const sp_layer* L) {
+  std::vector<HostChunk> hc(L->n_cc_chunks);
+  for (int k = 0; k < L->n_cc_chunks; ++k) {
+    const Chunk& ch = L->chunks[k];
+    const char* base = static_cast<const char*>(L->host) + ch.off;
+    hc[k] = HostChunk{base, L->d.gated ? base + ch.w3_off : nullptr, base + ch.w2_off, ch.r0, ch.rc};
+  }
+  return hc;
+}
+
+// x rows of a call gathered to fp32 [T, ldx] (zero padded) for the host CC kernel
+static void gather_host_x(float* xh, int64_t ldx, const void* x, int xdtype, int64_t M,
+                          const int32_t* ids, int64_t T) {
+  for (int64_t i = 0; i < T; ++i) {
+    const int64_t row = ids ? ids[i] : i;
+    if (xdtype == SP_BF16) {
+      const uint16_t* src = static_cast<const uint16_t*>(x) + row * M;
+      for (int64_t k = 0; k < M; ++k) {
+        const uint32_t u = uint32_t(src[k]) << 16;
+        memcpy(&xh[i * ldx + k], &u, 4);
+      }
+    } else {
+      memcpy(&xh[i * ldx], static_cast<const float*>(x) + row * M, size_t(M) * 4);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // forward
 
 static int forward_batch(Context* C, const sp_call* calls, int n_calls, const void* x, int xdtype,
                          int64_t T, void* y, int ydtype, unsigned flags, cudaStream_t user) {
   // ---- validate everything before enqueuing anything ----
-  if (n_calls < 0 || n_calls > kMaxMergeCalls)
-    return fail(SP_ERR_VALUE, "n_calls must lie in [0, %d], got %d", kMaxMergeCalls, n_calls);
+  if (n_calls < 1 || n_calls > kMaxCalls)
+    return fail(SP_ERR_VALUE, "n_calls must lie in [1, %d], got %d", kMaxCalls, n_calls);
   if (T < 1) return fail(SP_ERR_SHAPE, "input must have at least one row, got T=%lld", (long long)T);
   if ((xdtype != SP_F32 && xdtype != SP_BF16) || (ydtype != SP_F32 && ydtype != SP_BF16))
     return fail(SP_ERR_VALUE, "x/y dtype must be SP_F32 or SP_BF16");
@@ -485,7 +523,8 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
           return fail(SP_ERR_SHAPE, "call %d: token id %d outside [0, %lld)", c, k.token_ids[i],
                       (long long)T);
   }
-  if (n_calls == 0) return fail(SP_ERR_VALUE, "sp_forward_batch needs at least one call");
+  if (max_token_tile(M) == 0)
+    return fail(SP_ERR_VALUE, "model_dim %lld exceeds the %d-float x tile", (long long)M, kMaxTileFloats);
   const bool host_io = flags & SP_IO_HOST;
   const double t_call = now_s();
 
@@ -498,13 +537,15 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     dev_off += size_t(round_up(int64_t(bytes), 256));
     return o;
   };
-  std::vector<size_t> o_a(n_calls), o_y(n_calls), o_ycc(n_calls), o_ids(n_calls), o_g(n_calls);
+  std::vector<size_t> o_part(n_calls), o_y(n_calls), o_ycc(n_calls), o_ids(n_calls), o_g(n_calls);
   int64_t total_rows = 0;
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int64_t Te = calls[c].tokens;
-    ws[c].ldh = round_up(L->d.hidden_dim, kPadElems);
-    o_a[c] = dalloc(size_t(Te) * ws[c].ldh * 4);
+    int64_t slices = block_grid(C, L->h_gg);
+    for (int ci = 0; ci < int(L->chunks.size()); ++ci)
+      if (ci >= L->n_cc_chunks || calls[c].n_g > 0) slices += block_grid(C, L->chunks[ci].rc);
+    o_part[c] = dalloc(size_t(std::max<int64_t>(slices, 1)) * Te * N * 4);
     o_y[c] = dalloc(size_t(Te) * N * 4);
     o_ycc[c] = dalloc(size_t(Te) * N * 4);
     o_ids[c] = dalloc(size_t(Te) * 4);
@@ -517,7 +558,8 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   SP_TRY(C->ws.ensure(dev_off));
   char* dws = static_cast<char*>(C->ws.p);
   for (int c = 0; c < n_calls; ++c) {
-    ws[c].a = reinterpret_cast<float*>(dws + o_a[c]);
+    ws[c].part = reinterpret_cast<float*>(dws + o_part[c]);
+    ws[c].S = 0;
     ws[c].y = reinterpret_cast<float*>(dws + o_y[c]);
     ws[c].ycc = reinterpret_cast<float*>(dws + o_ycc[c]);
     ws[c].ids = reinterpret_cast<int32_t*>(dws + o_ids[c]);
@@ -555,8 +597,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         ids[i] = calls[c].token_ids ? calls[c].token_ids[i] : int32_t(i);
         g[i] = calls[c].gates ? calls[c].gates[i] : 1.0f;
       }
-      SP_CUDA(cudaMemcpyAsync(ws[c].ids, ids, Te * 4, cudaMemcpyHostToDevice, C->s_comp));
-      SP_CUDA(cudaMemcpyAsync(ws[c].gates, g, Te * 4, cudaMemcpyHostToDevice, C->s_comp));
+      if (Te > 0) {
+        SP_CUDA(cudaMemcpyAsync(ws[c].ids, ids, Te * 4, cudaMemcpyHostToDevice, C->s_comp));
+        SP_CUDA(cudaMemcpyAsync(ws[c].gates, g, Te * 4, cudaMemcpyHostToDevice, C->s_comp));
+      }
       mo += Te * 8;
     }
   }
@@ -583,20 +627,14 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int Te = int(calls[c].tokens);
-    if (Te == 0) continue;
-    if (L->h_gg > 0) {
-      BlockView b{static_cast<const char*>(L->gg), L->gg_w3_off, L->gg_w2_off, L->h_gg, L->ldm,
-                  L->ld_gg, L->d.b2};
-      GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, double(L->gg_bytes));
-      SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], 0, Te, false, C->s_comp));
-      span.end();
-    } else {
-      SP_CUDA(cudaMemsetAsync(ws[c].y, 0, size_t(Te) * N * 4, C->s_comp));
-    }
+    if (Te == 0 || L->h_gg <= 0) continue;
+    BlockView b{static_cast<const char*>(L->gg), L->gg_w3_off, L->gg_w2_off, L->h_gg};
+    GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, double(L->gg_bytes) * ((Te + 3) / 4));
+    SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], Te, 0, Te, C->s_comp));
+    span.end();
   }
 
   // ---- CG chunks (and CC chunks for the n_g diverted rows) through the ring ----
-  int chunk_seq = 0;
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int Te = int(calls[c].tokens);
@@ -618,16 +656,34 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       C->h2d_bytes += ch.bytes;
       SP_CUDA(cudaEventRecord(C->ev_copied[slot], C->s_copy));
       SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_copied[slot], 0));
-      BlockView b{static_cast<const char*>(C->ring[slot].p), ch.w3_off, ch.w2_off, ch.rc, L->ldm,
-                  ch.ldc, ch.r0};
+      BlockView b{static_cast<const char*>(C->ring[slot].p), ch.w3_off, ch.w2_off, ch.rc};
       const int t0 = is_cc ? Te - ng : 0;
       {
         GpuSpan span(C, C->s_comp, 2, is_cc ? SP_TRACE_CG_PRIME : SP_TRACE_CG, double(ch.bytes));
-        SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], t0, Te - t0, true, C->s_comp));
+        SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], Te, t0, Te - t0, C->s_comp));
         span.end();
       }
       SP_CUDA(cudaEventRecord(C->ev_free[slot], C->s_comp));
-      ++chunk_seq;
+    }
+  }
+
+  // ---- reduce every call's partial slices (fixed order) ----
+  {
+    ReduceArgs ra{};
+    ra.n_calls = n_calls;
+    ra.N = int(N);
+    ra.row_start[0] = 0;
+    for (int c = 0; c < n_calls; ++c) {
+      ra.c[c] = ReduceCall{ws[c].part, ws[c].y, ws[c].S, int(calls[c].tokens), 0};
+      ra.row_start[c + 1] = ra.row_start[c] + int(calls[c].tokens);
+    }
+    if (total_rows > 0) {
+      GpuSpan span(C, C->s_comp, 2, SP_TRACE_MERGE, 0.0);
+      dim3 grid(unsigned((N + 31) / 32), unsigned(total_rows));
+      reduce_slices_kernel<<<grid, 256, 0, C->s_comp>>>(ra);
+      SP_CUDA(cudaGetLastError());
+      ++C->launches;
+      span.end();
     }
   }
 
@@ -640,32 +696,12 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       const sp_layer* L = calls[c].layer;
       const int64_t Tcc = calls[c].tokens - calls[c].n_g;
       if (L->d.b1 <= 0 || Tcc <= 0) continue;
-      const int64_t ldx = round_up(M, kPadElems), lda = round_up(L->d.b1, kPadElems);
-      C->hscratch.assign(size_t(Tcc * ldx + Tcc * lda), 0.f);
-      float* xh = C->hscratch.data();
-      float* ah = xh + Tcc * ldx;
-      for (int64_t i = 0; i < Tcc; ++i) {
-        const int64_t row = calls[c].token_ids ? calls[c].token_ids[i] : i;
-        if (xdtype == SP_BF16) {
-          const uint16_t* src = static_cast<const uint16_t*>(x_host) + row * M;
-          for (int64_t k = 0; k < M; ++k) {
-            const uint32_t u = uint32_t(src[k]) << 16;
-            memcpy(&xh[i * ldx + k], &u, 4);
-          }
-        } else {
-          memcpy(&xh[i * ldx], static_cast<const float*>(x_host) + row * M, M * 4);
-        }
-      }
-      std::vector<HostChunk> hc(L->n_cc_chunks);
-      for (int k = 0; k < L->n_cc_chunks; ++k) {
-        const Chunk& ch = L->chunks[k];
-        const char* base = static_cast<const char*>(L->host) + ch.off;
-        hc[k] = HostChunk{base, L->d.gated ? base + ch.w3_off : nullptr, base + ch.w2_off, ch.r0,
-                          ch.rc, ch.ldc};
-      }
-      CCProblem pr{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, hc.data(), L->n_cc_chunks,
-                   L->d.b1, xh, ldx, Tcc, ah, lda,
-                   reinterpret_cast<float*>(hp + p_ycc[c])};
+      const int64_t ldx = round_up(M, kPadElems);
+      C->hscratch.assign(size_t(Tcc * ldx), 0.f);
+      gather_host_x(C->hscratch.data(), ldx, x_host, xdtype, M, calls[c].token_ids, Tcc);
+      std::vector<HostChunk> hc = host_cc_chunks(L);
+      CCProblem pr{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, L->ldn, hc.data(), L->n_cc_chunks,
+                   L->d.b1, C->hscratch.data(), ldx, Tcc, reinterpret_cast<float*>(hp + p_ycc[c])};
       cc_forward(pr, *C->pool, (flags & SP_NO_CC_THREADS) ? 1 : C->host_threads);
       host_span(C, 3, SP_TRACE_CC, t_cc0, now_s(), double(L->cc_bytes));
       SP_CUDA(cudaMemcpyAsync(ws[c].ycc, hp + p_ycc[c], size_t(Tcc) * N * 4, cudaMemcpyHostToDevice,
@@ -709,7 +745,6 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     SP_CUDA(cudaStreamWaitEvent(user, C->ev_done, 0));
   }
   if (C->trace.on) ++C->trace.call;
-  (void)chunk_seq;
   return SP_OK;
 }
 
@@ -801,9 +836,9 @@ int sp_shutdown(void) {
   return SP_OK;
 }
 
-int sp_layer_create(const sp_layer_desc* desc, const void* w1t, const void* w3t, const void* w2t,
+int sp_layer_create(const sp_layer_desc* desc, const void* w1t, const void* w3t, const void* w2,
                     sp_layer_t* out) {
-  if (!desc || !out || !w1t || !w2t) return fail(SP_ERR_VALUE, "NULL argument");
+  if (!desc || !out || !w1t || !w2) return fail(SP_ERR_VALUE, "NULL argument");
   const sp_layer_desc& d = *desc;
   if (d.model_dim < 1 || d.hidden_dim < 1 || d.out_dim < 1)
     return fail(SP_ERR_SHAPE, "layer dims must be >= 1 (M=%lld H=%lld N=%lld)", (long long)d.model_dim,
@@ -824,8 +859,9 @@ int sp_layer_create(const sp_layer_desc* desc, const void* w1t, const void* w3t,
   L->device = C->device;
   L->esz = d.wdtype == SP_BF16 ? 2 : 4;
   L->ldm = round_up(d.model_dim, kPadElems);
+  L->ldn = round_up(d.out_dim, kPadElems);
   L->host_only = C->host_only;
-  int st = pack_layer(L.get(), w1t, d.gated ? w3t : nullptr, w2t);
+  int st = pack_layer(L.get(), w1t, d.gated ? w3t : nullptr, w2);
   if (st != SP_OK) {
     if (L->gg) cudaFree(L->gg);
     if (L->host) L->host_only ? free(L->host) : (void)cudaFreeHost(L->host);
@@ -890,29 +926,14 @@ int sp_cc_forward_host(sp_layer_t L, const void* x, int xdtype, int64_t T, float
                        int threads) {
   if (!L || !x || !y_cc) return fail(SP_ERR_VALUE, "NULL argument");
   if (T < 0) return fail(SP_ERR_SHAPE, "negative token count");
+  if (xdtype != SP_F32 && xdtype != SP_BF16) return fail(SP_ERR_VALUE, "x dtype must be SP_F32 or SP_BF16");
   const int64_t M = L->d.model_dim, N = L->d.out_dim;
-  const int64_t ldx = round_up(M, kPadElems), lda = round_up(std::max<int64_t>(L->d.b1, 1), kPadElems);
-  std::vector<float> xh(size_t(T * ldx), 0.f), ah(size_t(T * lda), 0.f);
-  for (int64_t i = 0; i < T; ++i) {
-    if (xdtype == SP_BF16) {
-      const uint16_t* src = static_cast<const uint16_t*>(x) + i * M;
-      for (int64_t k = 0; k < M; ++k) {
-        const uint32_t u = uint32_t(src[k]) << 16;
-        memcpy(&xh[i * ldx + k], &u, 4);
-      }
-    } else {
-      memcpy(&xh[i * ldx], static_cast<const float*>(x) + i * M, M * 4);
-    }
-  }
-  std::vector<HostChunk> hc(L->n_cc_chunks);
-  for (int k = 0; k < L->n_cc_chunks; ++k) {
-    const Chunk& ch = L->chunks[k];
-    const char* base = static_cast<const char*>(L->host) + ch.off;
-    hc[k] = HostChunk{base, L->d.gated ? base + ch.w3_off : nullptr, base + ch.w2_off, ch.r0, ch.rc,
-                      ch.ldc};
-  }
-  CCProblem pr{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, hc.data(), L->n_cc_chunks, L->d.b1,
-               xh.data(), ldx, T, ah.data(), lda, y_cc};
+  const int64_t ldx = round_up(M, kPadElems);
+  std::vector<float> xh(size_t(T * ldx), 0.f);
+  gather_host_x(xh.data(), ldx, x, xdtype, M, nullptr, T);
+  std::vector<HostChunk> hc = host_cc_chunks(L);
+  CCProblem pr{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, L->ldn, hc.data(), L->n_cc_chunks,
+               L->d.b1, xh.data(), ldx, T, y_cc};
   Context* C = ctx_or_null();
   if (C && threads != 1) {
     cc_forward(pr, *C->pool, threads > 0 ? threads : C->host_threads);

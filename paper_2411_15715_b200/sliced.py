@@ -115,20 +115,23 @@ def _host_weights(a, code: int) -> np.ndarray:
 
 
 class NativeLayer:
-    """One FFN instance placed by libsliced (GG in HBM, CC/CG in pinned host)."""
+    """One FFN instance placed by libsliced (GG in HBM, CC/CG in pinned host).
 
-    def __init__(self, w1t, w2t, b1: int, b2: int, activation="silu", w3t=None,
+    w1t, w3t: [H, M] (the reference's w1 / w3 transposed: hidden unit h owns row
+    h); w2: [H, N] (the reference's own w2 layout)."""
+
+    def __init__(self, w1t, w2, b1: int, b2: int, activation="silu", w3t=None,
                  dtype: str = "bf16", chunk_rows: int = 0, device: int | None = None):
         code = _dtype_code(dtype)
         a1 = _host_weights(w1t, code)
-        a2 = _host_weights(w2t, code)
+        a2 = _host_weights(w2, code)
         a3 = None if w3t is None else _host_weights(w3t, code)
         if a1.ndim != 2 or a2.ndim != 2:
-            raise ShapeMismatch("w1t and w2t must be 2-D matrices")
+            raise ShapeMismatch("w1t and w2 must be 2-D matrices")
         hidden, model = a1.shape
-        out, hidden2 = a2.shape
+        hidden2, out = a2.shape
         if hidden2 != hidden:
-            raise ShapeMismatch(f"w1t has {hidden} rows but w2t has {hidden2} columns")
+            raise ShapeMismatch(f"w1t has {hidden} rows but w2 has {hidden2}; the hidden dim must match")
         if a3 is not None and a3.shape != a1.shape:
             raise ShapeMismatch(f"w3t is {a3.shape}, expected {a1.shape}")
         nat.init(device)
@@ -310,7 +313,7 @@ class SlicedWeights:
             w2 = np.concatenate(self.w2_blocks, axis=0)
             w3 = None if self.w3_blocks is None else np.concatenate(self.w3_blocks, axis=1)
             b1, b2 = self.boundaries
-            layer = NativeLayer(w1.T, w2.T, b1, b2, act, None if w3 is None else w3.T,
+            layer = NativeLayer(w1.T, w2, b1, b2, act, None if w3 is None else w3.T,
                                 dtype=self.dtype, chunk_rows=self.chunk_rows, device=device)
             self._placed[act] = layer
         return layer
@@ -459,7 +462,7 @@ class SlicedFFN:
                 raise ValueError("give rates or boundaries")
             boundaries = split_boundaries(hidden, rates)
         self.rates = rates
-        self.layer = NativeLayer(w1t, w2t, boundaries[0], boundaries[1], activation, w3t,
+        self.layer = NativeLayer(w1t, _transpose(w2t), boundaries[0], boundaries[1], activation, w3t,
                                  dtype=dtype, chunk_rows=chunk_rows, device=device)
 
     @property
@@ -472,6 +475,14 @@ class SlicedFFN:
         return forward_calls([CallSpec(self.layer, n_g=n_g)], x, out)
 
     __call__ = forward
+
+
+def _transpose(a):
+    """[N, H] -> contiguous [H, N] (torch's multi-threaded copy for tensors)."""
+    torch = _maybe_torch()
+    if torch is not None and isinstance(a, torch.Tensor):
+        return a.detach().t().contiguous()
+    return np.ascontiguousarray(np.asarray(a).T)
 
 
 def route_topk(logits: np.ndarray, k: int) -> tuple[np.ndarray, np.ndarray]:

@@ -68,12 +68,12 @@ def test_gpu_entry_points_refuse_without_device(host_ctx):
     from paper_2411_15715_b200.sliced import CallSpec, NativeLayer, forward_calls
 
     rng = np.random.default_rng(0)
-    lay = NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((8, 32)), 32, 32, "silu", dtype="f32")
+    lay = NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((32, 8)), 32, 32, "silu", dtype="f32")
     with pytest.raises(errors.NativeError, match="no CPU fallback"):
         forward_calls([CallSpec(lay)], rng.standard_normal((2, 16)))
     # a GG block cannot be placed without a device
     with pytest.raises(errors.NativeError):
-        NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((8, 32)), 0, 0, "silu", dtype="f32")
+        NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((32, 8)), 0, 0, "silu", dtype="f32")
 
 
 def test_layer_create_validates_like_the_reference(host_ctx):
@@ -81,9 +81,9 @@ def test_layer_create_validates_like_the_reference(host_ctx):
 
     rng = np.random.default_rng(1)
     with pytest.raises(errors.ShapeMismatch):
-        NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((8, 31)), 32, 32, dtype="f32")
+        NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((31, 8)), 32, 32, dtype="f32")
     with pytest.raises(ValueError):
-        NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((8, 32)), 20, 10, dtype="f32")
+        NativeLayer(rng.standard_normal((32, 16)), rng.standard_normal((32, 8)), 20, 10, dtype="f32")
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
@@ -96,7 +96,7 @@ def test_cc_host_kernel_matches_oracle(host_ctx, dtype, gated, act):
     for M, H, N, T, chunk in ((64, 200, 48, 5, 64), (100, 130, 20, 1, 64), (37, 300, 33, 9, 128)):
         w1, w3 = rng.uniform(-1, 1, (M, H)), rng.uniform(-1, 1, (M, H))
         w2, x = rng.uniform(-1, 1, (H, N)), rng.uniform(-1, 1, (T, M))
-        lay = NativeLayer(w1.T, w2.T, H, H, act, w3.T if gated else None, dtype=dtype, chunk_rows=chunk)
+        lay = NativeLayer(w1.T, w2, H, H, act, w3.T if gated else None, dtype=dtype, chunk_rows=chunk)
         got = lay.cc_forward_host(x, threads=3)
         q = orc.bf16_round if dtype == "bf16" else (lambda a: a)
         ref = orc.dense_forward(q(x), q(w1), q(w2), act, q(w3) if gated else None)
