@@ -152,6 +152,7 @@ struct FfnArgs {
   int t0, T;           // tokens [t0, t0 + T) of the call (T <= TT)
   int act;
   int kt;              // x tile: roundup(M, 256)
+  int xvec;            // x rows 16-byte aligned and M a multiple of the 16-byte vector
   // partial slices: part[(slice0 + blockIdx.x) * slice_stride + (t0 + t) * N + n]
   float* part;
   int64_t slice0, slice_stride;
@@ -229,17 +230,53 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
 
   // ---------------- consumers ----------------
   // stage x[:, 0:M) as fp32 (overlaps the first bulk copies); zero beyond M / T
-  for (int t = 0; t < TT; ++t) {
-    const bool live_t = t < p.T;
-    const int64_t row = live_t ? (p.ids ? p.ids[p.t0 + t] : int64_t(p.t0 + t)) : 0;
-    const int64_t base = row * p.ldx;
-    float* xrow = xs + t * p.kt;
-    for (int k = threadIdx.x; k < p.kt; k += kConsumers * 32) {
-      float v = 0.f;
-      if (live_t && k < p.M)
-        v = p.xdtype == 1 ? bf16_to_f(static_cast<const uint16_t*>(p.x)[base + k])
-                          : static_cast<const float*>(p.x)[base + k];
-      xrow[xs_pos<WT>(k, p.kt)] = v;
+  if (p.xvec) {
+    // 16-byte loads, all issued before any smem store (rows are 16-byte aligned, M % VX == 0)
+    const int vx = p.xdtype == 1 ? 8 : 4;
+    const int nvec = p.kt / vx;
+    constexpr int kPer = 4;
+    for (int i0 = threadIdx.x; i0 < TT * nvec; i0 += kPer * kConsumers * 32) {
+      uint4 raw[kPer];
+      int ks[kPer], ts[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = i0 + u * kConsumers * 32;
+        ts[u] = i / nvec;
+        ks[u] = (i - ts[u] * nvec) * vx;
+        raw[u] = make_uint4(0, 0, 0, 0);
+        if (i < TT * nvec && ts[u] < p.T && ks[u] < p.M) {
+          const int64_t row = p.ids ? p.ids[p.t0 + ts[u]] : int64_t(p.t0 + ts[u]);
+          const char* src = static_cast<const char*>(p.x) + (row * p.ldx + ks[u]) * (p.xdtype == 1 ? 2 : 4);
+          raw[u] = __ldg(reinterpret_cast<const uint4*>(src));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = i0 + u * kConsumers * 32;
+        if (i >= TT * nvec) break;
+        float* xrow = xs + ts[u] * p.kt;
+        float f[8];
+        if (vx == 8) {
+          unpack<__nv_bfloat16>(raw[u], f);
+        } else {
+          unpack<float>(raw[u], f);
+        }
+        for (int e = 0; e < vx; ++e) xrow[xs_pos<WT>(ks[u] + e, p.kt)] = f[e];
+      }
+    }
+  } else {
+    for (int t = 0; t < TT; ++t) {
+      const bool live_t = t < p.T;
+      const int64_t row = live_t ? (p.ids ? p.ids[p.t0 + t] : int64_t(p.t0 + t)) : 0;
+      const int64_t base = row * p.ldx;
+      float* xrow = xs + t * p.kt;
+      for (int k = threadIdx.x; k < p.kt; k += kConsumers * 32) {
+        float v = 0.f;
+        if (live_t && k < p.M)
+          v = p.xdtype == 1 ? bf16_to_f(static_cast<const uint16_t*>(p.x)[base + k])
+                            : static_cast<const float*>(p.x)[base + k];
+        xrow[xs_pos<WT>(k, p.kt)] = v;
+      }
     }
   }
   consumers_sync();

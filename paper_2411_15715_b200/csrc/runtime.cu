@@ -16,6 +16,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -135,6 +137,26 @@ struct Context {
   std::vector<float> hscratch;
   std::unique_ptr<ThreadPool> pool;
   int host_threads = 1;
+  // CC coordinator: runs a forward's CC block (on `pool`) while the calling
+  // thread keeps enqueueing GPU work -- Stream-A and Stream-B of PAPER.md:161
+  // on separate host threads.
+  std::thread cc_thread;
+  std::mutex cc_mu;
+  std::condition_variable cc_cv;
+  std::function<int()> cc_job;
+  bool cc_pending = false, cc_stop = false;
+  int cc_status = 0;
+  std::string cc_error;
+  std::mutex trace_mu;  // spans come from the calling thread and the coordinator
+
+  ~Context() {
+    {
+      std::lock_guard<std::mutex> lk(cc_mu);
+      cc_stop = true;
+      cc_cv.notify_all();
+    }
+    if (cc_thread.joinable()) cc_thread.join();
+  }
   std::mutex mu;
   Trace trace;
   std::map<std::pair<const void*, size_t>, int> occ_cache;
@@ -385,6 +407,12 @@ static int run_block(Context* C, const sp_layer* L, const BlockView& b, const vo
   a.ids = w.ids;
   a.act = L->d.act;
   a.kt = int(round_up(L->d.model_dim, 256));
+  {
+    const int vx = xdtype == SP_BF16 ? 8 : 4;
+    const size_t esz_x = xdtype == SP_BF16 ? 2 : 4;
+    a.xvec = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (ldx % vx == 0) &&
+             ((size_t(ldx) * esz_x) % 16 == 0) && (L->d.model_dim % vx == 0);
+  }
   a.part = w.part;
   a.slice0 = w.S;
   a.slice_stride = T_e * L->d.out_dim;
@@ -440,6 +468,7 @@ struct GpuSpan {
   void end() {
     if (!on) return;
     cudaEventRecord(sp.b, s);
+    std::lock_guard<std::mutex> g(C->trace_mu);
     C->trace.spans.push_back(sp);
     on = false;
   }
@@ -454,6 +483,7 @@ static void host_span(Context* C, int stream, int kind, double a, double b, doub
   sp.bytes = bytes;
   sp.ha = a - C->trace.host_t0;
   sp.hb = b - C->trace.host_t0;
+  std::lock_guard<std::mutex> g(C->trace_mu);
   C->trace.spans.push_back(sp);
 }
 
@@ -482,6 +512,39 @@ static void gather_host_x(float* xh, int64_t ldx, const void* x, int xdtype, int
       memcpy(&xh[i * ldx], static_cast<const float*>(x) + row * M, size_t(M) * 4);
     }
   }
+}
+
+static void cc_coordinator(Context* C) {
+  std::unique_lock<std::mutex> lk(C->cc_mu);
+  for (;;) {
+    C->cc_cv.wait(lk, [&] { return C->cc_stop || (C->cc_pending && C->cc_job); });
+    if (C->cc_stop) return;
+    std::function<int()> job = std::move(C->cc_job);
+    C->cc_job = nullptr;
+    lk.unlock();
+    const int st = job();
+    const std::string err = st == SP_OK ? std::string() : g_err;
+    lk.lock();
+    C->cc_status = st;
+    C->cc_error = err;
+    C->cc_pending = false;
+    C->cc_cv.notify_all();
+  }
+}
+
+static void cc_submit(Context* C, std::function<int()> job) {
+  std::lock_guard<std::mutex> g(C->cc_mu);
+  C->cc_job = std::move(job);
+  C->cc_pending = true;
+  C->cc_status = SP_OK;
+  C->cc_cv.notify_all();
+}
+
+static int cc_wait(Context* C) {
+  std::unique_lock<std::mutex> lk(C->cc_mu);
+  C->cc_cv.wait(lk, [&] { return !C->cc_pending; });
+  if (C->cc_status != SP_OK) return fail(C->cc_status, "%s", C->cc_error.c_str());
+  return SP_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -623,6 +686,31 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     x_host = hp + p_x;
   }
 
+  // ---- CC block: submitted to the coordinator now, runs while we enqueue ----
+  const bool cc_async = need_cc && !(flags & SP_NO_CC_THREADS);
+  auto cc_work = [=]() -> int {
+    if (!host_io) {
+      const cudaError_t e = cudaEventSynchronize(C->ev_x);
+      if (e != cudaSuccess) return fail(SP_ERR_CUDA, "x copy for the CC block: %s", cudaGetErrorString(e));
+    }
+    for (int c = 0; c < n_calls; ++c) {
+      const double t_cc0 = now_s();
+      const sp_layer* L = calls[c].layer;
+      const int64_t Tcc = calls[c].tokens - calls[c].n_g;
+      if (L->d.b1 <= 0 || Tcc <= 0) continue;
+      const int64_t ldx = round_up(M, kPadElems);
+      C->hscratch.assign(size_t(Tcc * ldx), 0.f);
+      gather_host_x(C->hscratch.data(), ldx, x_host, xdtype, M, calls[c].token_ids, Tcc);
+      std::vector<HostChunk> hc = host_cc_chunks(L);
+      CCProblem pr{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, L->ldn, hc.data(), L->n_cc_chunks,
+                   L->d.b1, C->hscratch.data(), ldx, Tcc, reinterpret_cast<float*>(hp + p_ycc[c])};
+      cc_forward(pr, *C->pool, (flags & SP_NO_CC_THREADS) ? 1 : C->host_threads);
+      host_span(C, 3, SP_TRACE_CC, t_cc0, now_s(), double(L->cc_bytes));
+    }
+    return SP_OK;
+  };
+  if (cc_async) cc_submit(C, cc_work);
+
   // ---- GG blocks (HBM resident) ----
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
@@ -658,6 +746,12 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_copied[slot], 0));
       BlockView b{static_cast<const char*>(C->ring[slot].p), ch.w3_off, ch.w2_off, ch.rc};
       const int t0 = is_cc ? Te - ng : 0;
+      if (t0 > 0) {
+        // a cg_prime block writes only rows [t0, Te) of its slices; the reducer sums every row
+        const size_t slice = size_t(Te) * N * 4;
+        SP_CUDA(cudaMemsetAsync(ws[c].part + size_t(ws[c].S) * Te * N, 0,
+                                slice * block_grid(C, ch.rc), C->s_comp));
+      }
       {
         GpuSpan span(C, C->s_comp, 2, is_cc ? SP_TRACE_CG_PRIME : SP_TRACE_CG, double(ch.bytes));
         SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], Te, t0, Te - t0, C->s_comp));
@@ -687,23 +781,13 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     }
   }
 
-  // ---- CC block on host threads (overlaps everything enqueued above) ----
+  // ---- join the CC block, ship its partials ----
   host_span(C, 0, SP_TRACE_LAUNCH, t_call, now_s(), 0.0);
   if (need_cc) {
-    if (!host_io) SP_CUDA(cudaEventSynchronize(C->ev_x));
+    SP_TRY(cc_async ? cc_wait(C) : cc_work());
     for (int c = 0; c < n_calls; ++c) {
-      const double t_cc0 = now_s();
-      const sp_layer* L = calls[c].layer;
       const int64_t Tcc = calls[c].tokens - calls[c].n_g;
-      if (L->d.b1 <= 0 || Tcc <= 0) continue;
-      const int64_t ldx = round_up(M, kPadElems);
-      C->hscratch.assign(size_t(Tcc * ldx), 0.f);
-      gather_host_x(C->hscratch.data(), ldx, x_host, xdtype, M, calls[c].token_ids, Tcc);
-      std::vector<HostChunk> hc = host_cc_chunks(L);
-      CCProblem pr{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, L->ldn, hc.data(), L->n_cc_chunks,
-                   L->d.b1, C->hscratch.data(), ldx, Tcc, reinterpret_cast<float*>(hp + p_ycc[c])};
-      cc_forward(pr, *C->pool, (flags & SP_NO_CC_THREADS) ? 1 : C->host_threads);
-      host_span(C, 3, SP_TRACE_CC, t_cc0, now_s(), double(L->cc_bytes));
+      if (calls[c].layer->d.b1 <= 0 || Tcc <= 0) continue;
       SP_CUDA(cudaMemcpyAsync(ws[c].ycc, hp + p_ycc[c], size_t(Tcc) * N * 4, cudaMemcpyHostToDevice,
                               C->s_aux));
     }
@@ -811,6 +895,8 @@ int sp_init(int device, int host_threads) {
   }
   C->host_threads = host_threads > 0 ? host_threads : std::max(1, hw);
   C->pool = std::make_unique<ThreadPool>(C->host_threads);
+  Context* raw = C.get();
+  C->cc_thread = std::thread([raw] { cc_coordinator(raw); });
   g_ctx = std::move(C);
   return SP_OK;
 }
@@ -823,6 +909,12 @@ int sp_shutdown(void) {
     g_ctx.reset();
     return SP_OK;
   }
+  {
+    std::lock_guard<std::mutex> lk(C->cc_mu);
+    C->cc_stop = true;
+    C->cc_cv.notify_all();
+  }
+  if (C->cc_thread.joinable()) C->cc_thread.join();
   cudaDeviceSynchronize();
   for (cudaEvent_t e : {C->ev_user, C->ev_x, C->ev_ycc, C->ev_done}) cudaEventDestroy(e);
   for (int i = 0; i < kRingSlots; ++i) {
