@@ -12,9 +12,9 @@
 //     a[t, h]   = act(<W1t[h], x[t]>) [* <W3t[h], x[t]>]            (phase 1)
 //     y_c[t, :] = sum_{h in CTA c's rows} a[t, h] * W2[h, :]          (phase 2)
 // and writes y_c -- CTA c's partial of the block's output -- to its own slice
-// of a partial buffer.  reduce_slices_kernel sums the slices of every block of
-// a call in a fixed order (deterministic), merge_kernel adds the CC partial,
-// applies the MoE gates and casts.  The up/down dependency therefore never
+// of a partial buffer.  finalize_kernel sums the slices of every block of a
+// call in a fixed order (deterministic), adds the CC partial, applies the MoE
+// gates and casts.  The up/down dependency therefore never
 // leaves the CTA: one launch per block, no grid-wide barrier, no `a` round trip.
 //
 // Decode is HBM-bound (~1 flop per weight byte).  Each CTA's rows are
@@ -137,6 +137,30 @@ __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
 }
 
+// Warp-reduce C values per lane (C a power of two <= 32) with (C - 1) + (5 - log2 C)
+// shuffles instead of 5 * C: every halving step swaps half of the values with
+// the partner lane (offset 16, 8, ...), then a plain butterfly finishes.  After
+// the call, value i's total is returned by every lane whose bits
+// [5 - log2 C, 5) equal i.
+template <int C>
+__device__ __forceinline__ float warp_reduce_transposed(float* v, int lane) {
+  int off = 16;
+#pragma unroll
+  for (int c = C; c > 1; c >>= 1, off >>= 1) {
+    const bool upper = lane & off;
+#pragma unroll
+    for (int i = 0; i < c / 2; ++i) {
+      const float send = upper ? v[i] : v[i + c / 2];
+      const float keep = upper ? v[i + c / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  float r = v[0];
+#pragma unroll
+  for (; off > 0; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+  return r;
+}
+
 struct FfnArgs {
   const void* w1t;     // [rows, ldm]
   const void* w3t;     // [rows, ldm] or null
@@ -171,6 +195,8 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
   constexpr int VE = VecTraits<WT>::kElems;
   constexpr int G = GATED ? 2 : 1;
   constexpr int STEP = 32 * VE;
+  // rows of a phase-1 stage reduced together (RSU * G * TT <= 32 values per lane)
+  constexpr int RSU = (2 * G * TT <= 32) ? 2 : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -292,18 +318,23 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
     mbar_wait(&full[slot], (s / NST) & 1);
     const int rows_s = min(fp.rs_up, n_local - s * fp.rs_up);
     const unsigned char* st = ring + size_t(slot) * fp.stage_bytes;
-    for (int j = 0; j < rows_s; ++j) {
-      float acc[G][TT];
+    // the stage's rows together: RSU x G x TT independent accumulators
+    for (int j0 = 0; j0 < rows_s; j0 += RSU) {
+      float acc[RSU * G * TT];
 #pragma unroll
-      for (int m = 0; m < G; ++m)
-#pragma unroll
-        for (int t = 0; t < TT; ++t) acc[m][t] = 0.f;
-#pragma unroll 4
+      for (int i = 0; i < RSU * G * TT; ++i) acc[i] = 0.f;
+      const bool live1 = RSU > 1 && j0 + 1 < rows_s;
+#pragma unroll 2
       for (int k = kb + lane * VE; k < ke; k += STEP) {
-        uint4 wv[G];
+        uint4 wv[RSU][G];
 #pragma unroll
-        for (int m = 0; m < G; ++m)
-          wv[m] = *reinterpret_cast<const uint4*>(st + (size_t(m) * fp.rs_up + j) * row1 + size_t(k) * sizeof(WT));
+        for (int j = 0; j < RSU; ++j)
+#pragma unroll
+          for (int m = 0; m < G; ++m)
+            wv[j][m] = (j == 0 || live1)
+                           ? *reinterpret_cast<const uint4*>(st + (size_t(m) * fp.rs_up + j0 + j) * row1 +
+                                                             size_t(k) * sizeof(WT))
+                           : make_uint4(0, 0, 0, 0);
         const int pos = xs_pos<WT>(k, p.kt);
 #pragma unroll
         for (int t = 0; t < TT; ++t) {
@@ -316,23 +347,27 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
             xv[4] = b.x; xv[5] = b.y; xv[6] = b.z; xv[7] = b.w;
           }
 #pragma unroll
-          for (int m = 0; m < G; ++m) {
-            float wf[VE];
-            unpack<WT>(wv[m], wf);
+          for (int j = 0; j < RSU; ++j)
 #pragma unroll
-            for (int e = 0; e < VE; ++e) acc[m][t] = fmaf(wf[e], xv[e], acc[m][t]);
-          }
+            for (int m = 0; m < G; ++m) {
+              float wf[VE];
+              unpack<WT>(wv[j][m], wf);
+              float& a_ = acc[(j * G + m) * TT + t];
+#pragma unroll
+              for (int e = 0; e < VE; ++e) a_ = fmaf(wf[e], xv[e], a_);
+            }
         }
       }
-#pragma unroll
-      for (int m = 0; m < G; ++m)
-#pragma unroll
-        for (int t = 0; t < TT; ++t) {
-          float v = acc[m][t];
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-          if (lane == 0) part1[(((s * fp.rs_up + j) * kConsumers + warp) * G + m) * TT + t] = v;
-        }
+      constexpr int CNT = RSU * G * TT;
+      constexpr int LOGC = CNT == 1 ? 0 : CNT == 2 ? 1 : CNT == 4 ? 2 : CNT == 8 ? 3 : CNT == 16 ? 4 : 5;
+      const float r = warp_reduce_transposed<CNT>(acc, lane);
+      constexpr int SHIFT = 5 - LOGC;
+      if ((lane & ((1 << SHIFT) - 1)) == 0) {
+        const int idx = lane >> SHIFT;  // (j * G + m) * TT + t
+        const int t = idx % TT, m = (idx / TT) % G, j = idx / (TT * G);
+        if (j == 0 || live1)
+          part1[(((s * fp.rs_up + j0 + j) * kConsumers + warp) * G + m) * TT + t] = r;
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
@@ -416,84 +451,74 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
   }
 }
 
-// ---- slice reduction: y_c[i, n] (+)= sum_s part_c[s, i, n], fixed order -------------
+// ---- finalize: slice reduction + CC partial + MoE gates + cast, one launch -------------
+//   y[t, n] = sum_c sum_{i: ids_c[i] = t} gate_c[i] * (sum_s part_c[s, i, n] + y_cc_c[i, n])
+// Block = 32 output columns x 8 slice groups.  Every column is owned by one
+// block and every sum runs in a fixed order, so results are deterministic.
 constexpr int kMaxCalls = 32;
-struct ReduceCall {
-  const float* part;  // [S][T_e][N]
-  float* y;           // [T_e][N]
-  int S, T_e;
-  int accumulate;
-};
-struct ReduceArgs {
-  ReduceCall c[kMaxCalls];
-  int row_start[kMaxCalls + 1];  // prefix sums of T_e
-  int n_calls;
-  int N;
-};
-
-// grid (ceil(N / 32), total rows); block 256 = 32 columns x 8 slice groups
-__global__ void __launch_bounds__(256) reduce_slices_kernel(ReduceArgs p) {
-  __shared__ float red[8][33];
-  const int row = blockIdx.y;
-  int c = 0;
-  while (c + 1 < p.n_calls && row >= p.row_start[c + 1]) ++c;
-  const ReduceCall& rc = p.c[c];
-  const int i = row - p.row_start[c];
-  const int col = threadIdx.x & 31, grp = threadIdx.x >> 5;
-  const int n = blockIdx.x * 32 + col;
-  float v = 0.f;
-  if (n < p.N)
-    for (int s = grp; s < rc.S; s += 8) v += rc.part[(int64_t(s) * rc.T_e + i) * p.N + n];
-  red[grp][col] = v;
-  __syncthreads();
-  if (grp == 0 && n < p.N) {
-    float tot = 0.f;
-#pragma unroll
-    for (int g = 0; g < 8; ++g) tot += red[g][col];
-    float* o = rc.y + int64_t(i) * p.N + n;
-    *o = rc.accumulate ? *o + tot : tot;
-  }
-}
-
-// ---- merge: y[t] = sum_c sum_{i: ids_c[i]=t} gate_c[i] * (y_gpu_c[i] + y_cc_c[i]) -------
-struct MergeCall {
-  const float* y_gpu;    // [T_e, N]
+struct FinalCall {
+  const float* part;     // [S][T_e][N] partial slices
+  int S;
   const float* y_cc;     // [T_e, N] or null; rows >= n_cc are absent
+  int n_cc;
   const int32_t* ids;    // device [T_e] or null (identity)
   const float* gates;    // device [T_e] or null (1.0)
   int T_e;
-  int n_cc;
 };
-struct MergeArgs {
-  MergeCall c[kMaxCalls];
+struct FinalArgs {
+  FinalCall c[kMaxCalls];
   int n_calls;
   int T;
-  int64_t N;
+  int N;
   float* acc;   // [T, N] fp32 scratch (also the output when odtype == f32)
   void* out;    // [T, N] in odtype
   int odtype;
 };
 
-__global__ void __launch_bounds__(256) merge_kernel(MergeArgs p) {
-  for (int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; n < p.N;
-       n += int64_t(gridDim.x) * blockDim.x) {
-    for (int t = 0; t < p.T; ++t) p.acc[t * p.N + n] = 0.f;
-    for (int c = 0; c < p.n_calls; ++c) {
-      const MergeCall& mc = p.c[c];
-      for (int i = 0; i < mc.T_e; ++i) {
-        const int t = mc.ids ? mc.ids[i] : i;
-        float v = mc.y_gpu[int64_t(i) * p.N + n];
-        if (mc.y_cc && i < mc.n_cc) v += mc.y_cc[int64_t(i) * p.N + n];
-        const float g = mc.gates ? mc.gates[i] : 1.0f;
-        p.acc[t * p.N + n] += g * v;
+__global__ void __launch_bounds__(256) finalize_kernel(FinalArgs p) {
+  __shared__ float red[8][33];
+  const int col = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int n = blockIdx.x * 32 + col;
+  const bool live = n < p.N;
+  if (grp == 0 && live)
+    for (int t = 0; t < p.T; ++t) p.acc[int64_t(t) * p.N + n] = 0.f;
+  for (int c = 0; c < p.n_calls; ++c) {
+    const FinalCall& fc = p.c[c];
+    for (int i = 0; i < fc.T_e; ++i) {
+      float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+      if (live) {
+        const float* base = fc.part + int64_t(i) * p.N + n;
+        const int64_t stride = int64_t(fc.T_e) * p.N;
+        int s = grp;
+        for (; s + 24 < fc.S; s += 32) {
+          v0 += base[int64_t(s) * stride];
+          v1 += base[int64_t(s + 8) * stride];
+          v2 += base[int64_t(s + 16) * stride];
+          v3 += base[int64_t(s + 24) * stride];
+        }
+        for (; s < fc.S; s += 8) v0 += base[int64_t(s) * stride];
       }
+      red[grp][col] = (v0 + v1) + (v2 + v3);
+      __syncthreads();
+      if (grp == 0 && live) {
+        float tot = 0.f;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) tot += red[g][col];
+        if (fc.y_cc && i < fc.n_cc) tot += fc.y_cc[int64_t(i) * p.N + n];
+        const int t = fc.ids ? fc.ids[i] : i;
+        const float gate = fc.gates ? fc.gates[i] : 1.0f;
+        p.acc[int64_t(t) * p.N + n] += gate * tot;
+      }
+      __syncthreads();
     }
+  }
+  if (grp == 0 && live) {
     if (p.odtype == 1) {
       __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out);
-      for (int t = 0; t < p.T; ++t) o[t * p.N + n] = __float2bfloat16_rn(p.acc[t * p.N + n]);
+      for (int t = 0; t < p.T; ++t) o[int64_t(t) * p.N + n] = __float2bfloat16_rn(p.acc[int64_t(t) * p.N + n]);
     } else if (p.out != p.acc) {
       float* o = static_cast<float*>(p.out);
-      for (int t = 0; t < p.T; ++t) o[t * p.N + n] = p.acc[t * p.N + n];
+      for (int t = 0; t < p.T; ++t) o[int64_t(t) * p.N + n] = p.acc[int64_t(t) * p.N + n];
     }
   }
 }

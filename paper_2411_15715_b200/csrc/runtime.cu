@@ -381,7 +381,6 @@ struct BlockView {
 struct CallWs {
   float* part;     // [S][T_e][N] partial slices of every block of the call
   int S;           // slices in use
-  float* y;        // [T_e, N] reduced GPU partial
   float* ycc;      // [T_e, N] CC partial (from the host)
   int32_t* ids;    // device
   float* gates;    // device
@@ -600,7 +599,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     dev_off += size_t(round_up(int64_t(bytes), 256));
     return o;
   };
-  std::vector<size_t> o_part(n_calls), o_y(n_calls), o_ycc(n_calls), o_ids(n_calls), o_g(n_calls);
+  std::vector<size_t> o_part(n_calls), o_ycc(n_calls), o_ids(n_calls), o_g(n_calls);
   int64_t total_rows = 0;
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
@@ -609,7 +608,6 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     for (int ci = 0; ci < int(L->chunks.size()); ++ci)
       if (ci >= L->n_cc_chunks || calls[c].n_g > 0) slices += block_grid(C, L->chunks[ci].rc);
     o_part[c] = dalloc(size_t(std::max<int64_t>(slices, 1)) * Te * N * 4);
-    o_y[c] = dalloc(size_t(Te) * N * 4);
     o_ycc[c] = dalloc(size_t(Te) * N * 4);
     o_ids[c] = dalloc(size_t(Te) * 4);
     o_g[c] = dalloc(size_t(Te) * 4);
@@ -623,7 +621,6 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   for (int c = 0; c < n_calls; ++c) {
     ws[c].part = reinterpret_cast<float*>(dws + o_part[c]);
     ws[c].S = 0;
-    ws[c].y = reinterpret_cast<float*>(dws + o_y[c]);
     ws[c].ycc = reinterpret_cast<float*>(dws + o_ycc[c]);
     ws[c].ids = reinterpret_cast<int32_t*>(dws + o_ids[c]);
     ws[c].gates = reinterpret_cast<float*>(dws + o_g[c]);
@@ -761,26 +758,6 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     }
   }
 
-  // ---- reduce every call's partial slices (fixed order) ----
-  {
-    ReduceArgs ra{};
-    ra.n_calls = n_calls;
-    ra.N = int(N);
-    ra.row_start[0] = 0;
-    for (int c = 0; c < n_calls; ++c) {
-      ra.c[c] = ReduceCall{ws[c].part, ws[c].y, ws[c].S, int(calls[c].tokens), 0};
-      ra.row_start[c + 1] = ra.row_start[c] + int(calls[c].tokens);
-    }
-    if (total_rows > 0) {
-      GpuSpan span(C, C->s_comp, 2, SP_TRACE_MERGE, 0.0);
-      dim3 grid(unsigned((N + 31) / 32), unsigned(total_rows));
-      reduce_slices_kernel<<<grid, 256, 0, C->s_comp>>>(ra);
-      SP_CUDA(cudaGetLastError());
-      ++C->launches;
-      span.end();
-    }
-  }
-
   // ---- join the CC block, ship its partials ----
   host_span(C, 0, SP_TRACE_LAUNCH, t_call, now_s(), 0.0);
   if (need_cc) {
@@ -795,26 +772,24 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_ycc, 0));
   }
 
-  // ---- merge ----
-  MergeArgs ma{};
-  ma.n_calls = n_calls;
-  ma.T = int(T);
-  ma.N = N;
-  ma.acc = reinterpret_cast<float*>(dws + o_acc);
-  ma.out = host_io ? static_cast<void*>(dws + o_ydev) : y;
-  ma.odtype = ydtype;
+  // ---- finalize: reduce slices + CC partials + gates + cast ----
+  FinalArgs fa{};
+  fa.n_calls = n_calls;
+  fa.T = int(T);
+  fa.N = int(N);
+  fa.acc = reinterpret_cast<float*>(dws + o_acc);
+  fa.out = host_io ? static_cast<void*>(dws + o_ydev) : y;
+  fa.odtype = ydtype;
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int64_t Tcc = calls[c].tokens - calls[c].n_g;
-    ma.c[c] = MergeCall{ws[c].y, (L->d.b1 > 0 && Tcc > 0) ? ws[c].ycc : nullptr, ws[c].ids,
-                        ws[c].gates, int(calls[c].tokens), int(Tcc)};
+    fa.c[c] = FinalCall{ws[c].part, ws[c].S, (L->d.b1 > 0 && Tcc > 0) ? ws[c].ycc : nullptr, int(Tcc),
+                        ws[c].ids, ws[c].gates, int(calls[c].tokens)};
   }
-  if (ydtype == SP_F32 && !host_io) ma.acc = static_cast<float*>(y);
+  if (ydtype == SP_F32 && !host_io) fa.acc = static_cast<float*>(y);
   {
-    const int threads = 256;
-    const int blocks = int(std::min<int64_t>((N + threads - 1) / threads, int64_t(C->num_sms) * 4));
     GpuSpan span(C, C->s_comp, 2, SP_TRACE_MERGE, 0.0);
-    merge_kernel<<<blocks, threads, 0, C->s_comp>>>(ma);
+    finalize_kernel<<<unsigned((N + 31) / 32), 256, 0, C->s_comp>>>(fa);
     SP_CUDA(cudaGetLastError());
     span.end();
     ++C->launches;
