@@ -180,7 +180,18 @@ struct FfnArgs {
   // partial slices: part[(slice0 + blockIdx.x) * slice_stride + (t0 + t) * N + n]
   float* part;
   int64_t slice0, slice_stride;
+  unsigned long long* stamps;  // debug timing: [grid][8] %globaltimer stamps, or null
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SP_STAMP(i)                                                            \
+  do {                                                                         \
+    if (p.stamps && threadIdx.x == 0) p.stamps[blockIdx.x * 8 + (i)] = global_ns(); \
+  } while (0)
 
 struct FfnPlan {
   int rs_up;        // hidden rows per phase-1 stage
@@ -200,6 +211,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
   extern __shared__ __align__(128) unsigned char smem_raw[];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  SP_STAMP(0);
   const int64_t r_begin = (int64_t)p.rows * blockIdx.x / gridDim.x;
   const int64_t r_end = (int64_t)p.rows * (blockIdx.x + 1) / gridDim.x;
   const int n_local = int(r_end - r_begin);
@@ -223,6 +235,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  SP_STAMP(1);
 
   if (warp == kConsumers) {
     // ---------------- producer: one lane streams the CTA's rows ----------------
@@ -306,6 +319,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
     }
   }
   consumers_sync();
+  SP_STAMP(2);
 
   // ---- phase 1: a[t, h] for the CTA's rows ----
   // vectors [k, k + VE) with k < M stay inside the zero-padded row and meet zero x beyond M
@@ -373,6 +387,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
     if (lane == 0) mbar_arrive(&empty[slot]);
   }
   consumers_sync();
+  SP_STAMP(3);
   for (int i = threadIdx.x; i < n_local * TT; i += kConsumers * 32) {
     const int lr = i / TT, t = i - lr * TT;
     float v[G];
@@ -387,6 +402,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
     a_loc[lr * TT + t] = t < p.T ? a : 0.f;
   }
   consumers_sync();
+  SP_STAMP(4);
 
   // ---- phase 2: y_c[t, :] = sum_h a[t, h] * W2[h, :] ----
   const int tid = threadIdx.x;
@@ -426,6 +442,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
   }
+  SP_STAMP(5);
   // write this CTA's partial slice (a CTA with no rows writes zeros)
   float* out = p.part + (p.slice0 + blockIdx.x) * p.slice_stride;
 #pragma unroll
@@ -449,6 +466,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
       }
     }
   }
+  SP_STAMP(6);
 }
 
 // ---- finalize: slice reduction + CC partial + MoE gates + cast, one launch -------------

@@ -161,6 +161,7 @@ struct Context {
   Trace trace;
   std::map<std::pair<const void*, size_t>, int> occ_cache;
   uint64_t launches = 0, h2d_bytes = 0;
+  unsigned long long* stamps = nullptr;  // SP_KSTAMPS=1: per-CTA %globaltimer stamps of ffn_block
 };
 
 static std::mutex g_ctx_mu;
@@ -413,6 +414,7 @@ static int run_block(Context* C, const sp_layer* L, const BlockView& b, const vo
              ((size_t(ldx) * esz_x) % 16 == 0) && (L->d.model_dim % vx == 0);
   }
   a.part = w.part;
+  a.stamps = C->stamps;
   a.slice0 = w.S;
   a.slice_stride = T_e * L->d.out_dim;
   for (int tb = 0; tb < T; tb += tt_max) {
@@ -872,6 +874,10 @@ int sp_init(int device, int host_threads) {
   C->pool = std::make_unique<ThreadPool>(C->host_threads);
   Context* raw = C.get();
   C->cc_thread = std::thread([raw] { cc_coordinator(raw); });
+  if (env_int("SP_KSTAMPS", 0)) {
+    SP_CUDA(cudaMalloc(&C->stamps, 4096 * 8 * sizeof(unsigned long long)));
+    SP_CUDA(cudaMemset(C->stamps, 0, 4096 * 8 * sizeof(unsigned long long)));
+  }
   g_ctx = std::move(C);
   return SP_OK;
 }
@@ -1076,6 +1082,15 @@ int sp_stats(uint64_t* kernel_launches, uint64_t* h2d_bytes) {
   if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
   if (kernel_launches) *kernel_launches = C->launches;
   if (h2d_bytes) *h2d_bytes = C->h2d_bytes;
+  return SP_OK;
+}
+
+// Internal (not in sliced.h): copy the last ffn_block launch's per-CTA stamps.
+int sp_debug_stamps(unsigned long long* out, int n) {
+  Context* C = ctx_or_null();
+  if (!C || !C->stamps) return fail(SP_ERR_STATE, "stamps disabled (set SP_KSTAMPS=1)");
+  SP_CUDA(cudaDeviceSynchronize());
+  SP_CUDA(cudaMemcpy(out, C->stamps, size_t(std::min(n, 4096 * 8)) * 8, cudaMemcpyDeviceToHost));
   return SP_OK;
 }
 
