@@ -177,6 +177,7 @@ struct FfnArgs {
   int act;
   int kt;              // x tile: roundup(M, 256)
   int xvec;            // x rows 16-byte aligned and M a multiple of the 16-byte vector
+  int tok[4];          // x rows of the launch's tokens (host-resolved ids), used when xvec
   // partial slices: part[(slice0 + blockIdx.x) * slice_stride + (t0 + t) * N + n]
   float* part;
   int64_t slice0, slice_stride;
@@ -200,7 +201,8 @@ struct FfnPlan {
   int stage_bytes;  // bytes per ring slot
 };
 
-// smem: ring[NST][stage] | xs[TT][kt] | part1[n_local][8][G][TT] | a_loc[n_local][TT] | bars
+// smem: ring[NST][stage] | xs[TT][kt] | xraw[TT][M] (xvec) | part1[n_local][8][G][TT] |
+//       a_loc[n_local][TT] | full[NST] | empty[NST] | xbar
 template <typename WT, int TT, bool GATED, int NV>
 __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, FfnPlan fp) {
   constexpr int VE = VecTraits<WT>::kElems;
@@ -220,25 +222,39 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
   const int n_dn = (n_local + fp.rs_down - 1) / fp.rs_down;
   const int64_t row1 = p.ldm * int64_t(sizeof(WT)), row2 = p.ldn * int64_t(sizeof(WT));
 
+  const int xel = p.xdtype == 1 ? 2 : 4;
+  const int xraw_bytes = p.xvec ? (TT * p.M * xel + 15) / 16 * 16 : 0;
   unsigned char* ring = smem_raw;
   float* xs = reinterpret_cast<float*>(ring + size_t(NST) * fp.stage_bytes);
-  float* part1 = xs + TT * p.kt;
+  unsigned char* xraw = reinterpret_cast<unsigned char*>(xs + TT * p.kt);
+  float* part1 = reinterpret_cast<float*>(xraw + xraw_bytes);
   float* a_loc = part1 + n_local * kConsumers * G * TT;
   uint64_t* full = reinterpret_cast<uint64_t*>(a_loc + ((n_local * TT + 1) & ~1));
   uint64_t* empty = full + NST;
+  uint64_t* xbar = empty + NST;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers);
     }
+    mbar_init(xbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   SP_STAMP(1);
 
   if (warp == kConsumers) {
-    // ---------------- producer: one lane streams the CTA's rows ----------------
+    // ---------------- producer: one lane streams x, then the CTA's rows ----------------
+    if (lane == 0 && p.xvec) {
+      // x first: a load issued behind the weight stream would wait for ~NST stages per SM
+      const uint32_t row_bytes_x = uint32_t(p.M * xel);
+      mbar_expect_tx(xbar, row_bytes_x * p.T);
+      for (int t = 0; t < p.T; ++t)
+        bulk_g2s(xraw + size_t(t) * row_bytes_x,
+                 static_cast<const char*>(p.x) + int64_t(p.tok[t]) * p.ldx * xel, row_bytes_x, xbar,
+                 evict_first_policy());
+    }
     if (lane == 0 && n_local > 0) {
       const uint64_t pol = evict_first_policy();
       const char* s1 = static_cast<const char*>(p.w1t) + r_begin * row1;
@@ -268,40 +284,23 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
   }
 
   // ---------------- consumers ----------------
-  // stage x[:, 0:M) as fp32 (overlaps the first bulk copies); zero beyond M / T
+  // x -> fp32 tile xs (zero beyond M and beyond T)
   if (p.xvec) {
-    // 16-byte loads, all issued before any smem store (rows are 16-byte aligned, M % VX == 0)
+    mbar_wait(xbar, 0);
     const int vx = p.xdtype == 1 ? 8 : 4;
     const int nvec = p.kt / vx;
-    constexpr int kPer = 4;
-    for (int i0 = threadIdx.x; i0 < TT * nvec; i0 += kPer * kConsumers * 32) {
-      uint4 raw[kPer];
-      int ks[kPer], ts[kPer];
+    for (int i = threadIdx.x; i < TT * nvec; i += kConsumers * 32) {
+      const int t = i / nvec, k = (i - t * nvec) * vx;
+      float f[8];
+      if (t < p.T && k < p.M) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(xraw + (size_t(t) * p.M + k) * xel);
+        if (vx == 8) unpack<__nv_bfloat16>(raw, f); else unpack<float>(raw, f);
+      } else {
 #pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int i = i0 + u * kConsumers * 32;
-        ts[u] = i / nvec;
-        ks[u] = (i - ts[u] * nvec) * vx;
-        raw[u] = make_uint4(0, 0, 0, 0);
-        if (i < TT * nvec && ts[u] < p.T && ks[u] < p.M) {
-          const int64_t row = p.ids ? p.ids[p.t0 + ts[u]] : int64_t(p.t0 + ts[u]);
-          const char* src = static_cast<const char*>(p.x) + (row * p.ldx + ks[u]) * (p.xdtype == 1 ? 2 : 4);
-          raw[u] = __ldg(reinterpret_cast<const uint4*>(src));
-        }
+        for (int e = 0; e < 8; ++e) f[e] = 0.f;
       }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int i = i0 + u * kConsumers * 32;
-        if (i >= TT * nvec) break;
-        float* xrow = xs + ts[u] * p.kt;
-        float f[8];
-        if (vx == 8) {
-          unpack<__nv_bfloat16>(raw[u], f);
-        } else {
-          unpack<float>(raw[u], f);
-        }
-        for (int e = 0; e < vx; ++e) xrow[xs_pos<WT>(ks[u] + e, p.kt)] = f[e];
-      }
+      float* xrow = xs + t * p.kt;
+      for (int e = 0; e < vx; ++e) xrow[xs_pos<WT>(k + e, p.kt)] = f[e];
     }
   } else {
     for (int t = 0; t < TT; ++t) {

@@ -340,8 +340,9 @@ static int launch_ffn_t(Context* C, const FfnArgs& a, int grid, cudaStream_t s) 
   rs_up = std::min(rs_up, per_cta);
   rs_dn = std::min(rs_dn, per_cta);
   const size_t stage = size_t(std::max<int64_t>(G * rs_up * row1, rs_dn * row2));
-  const size_t fixed = size_t(TT) * a.kt * 4 + size_t(per_cta) * kConsumers * G * TT * 4 +
-                       size_t((per_cta * TT + 1) & ~1) * 4 + 2 * kMaxStages * 8 + 128;
+  const size_t xraw = a.xvec ? size_t((TT * a.M * (a.xdtype == 1 ? 2 : 4) + 15) / 16 * 16) : 0;
+  const size_t fixed = size_t(TT) * a.kt * 4 + xraw + size_t(per_cta) * kConsumers * G * TT * 4 +
+                       size_t((per_cta * TT + 1) & ~1) * 4 + (2 * kMaxStages + 1) * 8 + 128;
   if (fixed + 2 * stage > size_t(kSmemLimit))
     return fail(SP_ERR_VALUE, "block of %d rows (M=%d, N=%d) does not fit shared memory", a.rows, a.M, a.N);
   const int nst = int(std::min<size_t>(g_max_stages, (kSmemLimit - fixed) / stage));
@@ -388,7 +389,8 @@ struct CallWs {
 };
 
 static int run_block(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,
-                     int64_t ldx, CallWs& w, int64_t T_e, int t0, int T, cudaStream_t s) {
+                     int64_t ldx, CallWs& w, const int32_t* host_ids, int64_t T_e, int t0, int T,
+                     cudaStream_t s) {
   const int grid = block_grid(C, b.rows);
   const int tt_max = max_token_tile(L->d.model_dim);
   if (tt_max == 0) return fail(SP_ERR_VALUE, "model_dim %lld exceeds the x tile", (long long)L->d.model_dim);
@@ -422,6 +424,10 @@ static int run_block(Context* C, const sp_layer* L, const BlockView& b, const vo
     const int tt = n <= 1 ? 1 : n <= 2 ? 2 : 4;
     a.t0 = t0 + tb;
     a.T = n;
+    for (int t = 0; t < 4; ++t) {
+      const int64_t i = std::min<int64_t>(a.t0 + t, T_e - 1);
+      a.tok[t] = host_ids ? host_ids[i] : int32_t(i);
+    }
     int st;
     if (L->d.wdtype == SP_BF16)
       st = L->d.gated ? launch_tt<__nv_bfloat16, true>(C, tt, a, grid, s)
@@ -717,7 +723,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     if (Te == 0 || L->h_gg <= 0) continue;
     BlockView b{static_cast<const char*>(L->gg), L->gg_w3_off, L->gg_w2_off, L->h_gg};
     GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, double(L->gg_bytes) * ((Te + 3) / 4));
-    SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], Te, 0, Te, C->s_comp));
+    SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, 0, Te, C->s_comp));
     span.end();
   }
 
@@ -753,7 +759,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       }
       {
         GpuSpan span(C, C->s_comp, 2, is_cc ? SP_TRACE_CG_PRIME : SP_TRACE_CG, double(ch.bytes));
-        SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], Te, t0, Te - t0, C->s_comp));
+        SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, t0, Te - t0, C->s_comp));
         span.end();
       }
       SP_CUDA(cudaEventRecord(C->ev_free[slot], C->s_comp));
