@@ -3,26 +3,28 @@
 
 Default workload (BASELINE.json configs[1]): one Mixtral-8x7B MoE FFN layer
 (model 4096, ffn 14336, 8 SwiGLU experts, top-2, bf16), decode, batch 1 token
-per step, with slicing rates chosen by the partition API on the re-fitted
+per step per GPU, slicing rates chosen by the partition API on the re-fitted
 B200 profile (profiles/b200_decode.json) under an explicit GPU byte budget
 (default: half of every expert resident in HBM, the paper's limited-memory
-regime).  A step = route the token(s), run every active
-expert's GG block (HBM), stream its CG block over PCIe through the HBM ring,
-compute its CC block on the host threads, merge.
+regime).  A step = route the token(s), run every active expert's GG block
+(HBM), stream its CG block over PCIe through the HBM ring, compute its CC block
+on the host threads, merge (and all-reduce over ranks when N > 1).
 
-Lines (one JSON line on rank 0):
-  value    tokens/s with x resident in HBM (SP_IO_DEVICE)
+``--config cfg1``: BASELINE configs[0] shapes (1024/3584, fp32, fixed rates
+0.2/0.3/0.5) through the same runtime.
+
+Keys of the JSON line (rank 0):
+  value    tokens/s with x resident in HBM (SP_IO_DEVICE), CUDA events, max over ranks
   e2e      tokens/s through the public API with host x / y (SP_IO_HOST)
-  roofline GG GEMV pair (dominant kernel) achieved HBM GB/s vs MEASURED_PEAKS
-  link     CG copy GB/s vs the measured pinned H2D peak, and the step roofline
-           t_roof = max(GG bytes / HBM, CG bytes / link) over the measured step
+  roofline GG ffn_block launch (dominant HBM kernel) achieved GB/s vs MEASURED_PEAKS
+  link     CG copy GB/s vs the measured link, and the step roofline
+           t_roof = max(GG bytes / HBM, CG bytes / link) / measured step
   cpu_baseline  the reference algorithm (oracle/sliced_forward.py, fp64 numpy,
            slicing_kernel.py:97-124) on the host cores, bounded sample
 
 ``--impl reference`` times that CPU reference alone on the same config.
-Multi-GPU (torchrun): experts are sharded round-robin over ranks, each rank
-with its own GG/CG/CC split and host link; the per-rank outputs are summed
-with one NCCL all-reduce; global batch = batch * world (weak scaling).
+Multi-GPU (torchrun): experts are sharded round-robin (expert_parallel.py),
+one NCCL all-reduce per step; global batch = batch * world (weak scaling).
 """
 
 from __future__ import annotations
@@ -41,28 +43,37 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "decode tokens/s, Mixtral-8x7B MoE FFN layer (4096/14336, 8 experts top-2), sliced CC/CG/GG"
 UNIT = "tokens/s"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2"])
     ap.add_argument("--batch", type=int, default=1, help="decode tokens per step per GPU")
     ap.add_argument("--budget-frac", type=float, default=0.5,
                     help="GPU budget as a fraction of each expert's bytes (planner units)")
     ap.add_argument("--experts", type=int, default=8)
-    ap.add_argument("--model-dim", type=int, default=4096)
-    ap.add_argument("--hidden-dim", type=int, default=14336)
     ap.add_argument("--top-k", type=int, default=2)
     ap.add_argument("--profile", default=str(ROOT / "profiles" / "b200_decode.json"))
     ap.add_argument("--cpu-sample-steps", type=int, default=6)
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.config == "cfg1":
+        args.model_dim, args.hidden_dim, args.dtype = 1024, 3584, "f32"
+    else:
+        args.model_dim, args.hidden_dim, args.dtype = 4096, 14336, "bf16"
+    return args
+
+
+def metric_name(args):
+    if args.config == "cfg1":
+        return "decode tokens/s, MoE FFN layer 1024/3584 (8 experts top-2) fp32, fixed CC/CG/GG 0.2/0.3/0.5"
+    return "decode tokens/s, Mixtral-8x7B MoE FFN layer (4096/14336, 8 experts top-2), sliced CC/CG/GG"
 
 
 # ---------------------------------------------------------------------------
@@ -80,16 +91,18 @@ def load_profile(path):
 
 
 def plan_rates(args, tokens_per_step):
-    """greedy_assign under the budget picks r_GG, solve_rcg the best r_CG."""
+    """greedy_assign under the budget picks r_GG, solve_rcg the best r_CG
+    (config 1 uses the fixed rates of BASELINE.json configs[0])."""
     import paper_2411_15715_b200 as sp
 
     profile, source = load_profile(args.profile)
     layer = sp.LayerSpec(args.model_dim, args.hidden_dim, n_gemms=args.top_k * 3, precision=sp.Precision.FP16)
-    wl = sp.Workload(tokens=tokens_per_step, phase=sp.Phase.GENERATION)
     budget = args.budget_frac * layer.layer_bytes
+    if args.config == "cfg1":
+        return sp.SlicingRates(0.2, 0.3, 0.5), budget, "fixed 0.2/0.3/0.5 (BASELINE configs[0])", profile
+    wl = sp.Workload(tokens=tokens_per_step, phase=sp.Phase.GENERATION)
     mem = sp.greedy_assign(profile, [layer], wl, budget, n_steps=16)
-    sol = sp.solve_rcg(profile, layer, wl, mem.per_layer_rgg[0])
-    return sol, layer, budget, source, profile
+    return sp.solve_rcg(profile, layer, wl, mem.per_layer_rgg[0]).rates, budget, source, profile
 
 
 # ---------------------------------------------------------------------------
@@ -97,19 +110,21 @@ def plan_rates(args, tokens_per_step):
 
 
 class ClockSampler:
-    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device=0):
-        self.rows, self.proc, self.device = [], None, device
+        self.rows, self.proc, self.device, self.armed = [], None, device, False
+        self.first = threading.Event()
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+            self.first.wait(timeout=10)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -118,20 +133,22 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.first.set()
+                if self.armed:
+                    self.rows.append(parts)
 
-    def __exit__(self, *a):
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        num = lambda v: float(v) if v.replace(".", "").isdigit() else None  # noqa: E731
+        sm = [v for v in (num(r[0]) for r in self.rows) if v is not None]
+        mx = [v for v in (num(r[1]) for r in self.rows) if v is not None]
+        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:]) if v.lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
 
@@ -141,20 +158,18 @@ class ClockSampler:
 
 
 def cpu_reference_sample(args, rates, steps, warmup=1):
-    """fp64 numpy sliced forward of the reference algorithm for `batch` tokens
-    through top-k experts (two fp64 weight sets, 2.8 GB > L3, reused across
-    steps); returns (tokens/s, seconds/step, description)."""
+    """fp64 numpy sliced forward (the reference algorithm) of `batch` tokens
+    through top-k SwiGLU experts; two fp64 expert weight sets (> L3) reused
+    across steps.  Returns (tokens/s, s/step, description, threads)."""
     import torch
 
     from oracle import sliced_forward as orc
 
     M, H = args.model_dim, args.hidden_dim
     torch.manual_seed(0)
-    sets = []
-    for _ in range(min(2, args.top_k)):
-        sets.append(tuple((torch.randn(*s) / 64).double().numpy() for s in ((M, H), (M, H), (H, M))))
-    rng = np.random.default_rng(0)
-    x = rng.standard_normal((args.batch, M))
+    sets = [tuple((torch.randn(*s) / 64).double().numpy() for s in ((M, H), (M, H), (H, M)))
+            for _ in range(min(2, args.top_k))]
+    x = np.random.default_rng(0).standard_normal((args.batch, M))
     gates = np.full(args.top_k, 1.0 / args.top_k)
 
     def step():
@@ -176,8 +191,9 @@ def cpu_reference_sample(args, rates, steps, warmup=1):
         threads = max(i.get("num_threads", 1) for i in threadpoolctl.threadpool_info() if i.get("user_api") == "blas")
     except Exception:
         threads = os.cpu_count()
-    desc = (f"{steps} steps x {args.batch} token(s) x {args.top_k} experts, fp64 numpy/OpenBLAS, "
-            f"rates cc={rates.cc:.4f} cg={rates.cg:.4f} gg={rates.gg:.4f}, 2 fp64 expert weight sets")
+    desc = (f"{steps} steps x {args.batch} token(s) x {args.top_k} experts, fp64 numpy/OpenBLAS "
+            f"(slicing_kernel.py:97-124 as written), rates cc={rates.cc:.4f} cg={rates.cg:.4f} gg={rates.gg:.4f}, "
+            f"2 fp64 expert weight sets")
     return args.batch / dt, dt, desc, threads
 
 
@@ -185,73 +201,61 @@ def cpu_reference_sample(args, rates, steps, warmup=1):
 
 
 def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def base_config(args, rates, global_batch, world):
+    return {"workload": f"{'mixtral-8x7b' if args.config == 'cfg2' else 'cfg1-1024x3584'}-moe-ffn-decode",
+            "model_dim": args.model_dim, "hidden_dim": args.hidden_dim, "experts": args.experts,
+            "top_k": args.top_k, "batch_per_gpu": args.batch, "global_batch": global_batch,
+            "parallelism": f"ep{world}" if world > 1 else "single",
+            "rates": {"cc": rates.cc, "cg": rates.cg, "gg": rates.gg}}
 
 
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    sol, layer, budget, source, _ = plan_rates(args, args.batch)
-    per_step = []
+    rates, _, _, _ = plan_rates(args, args.batch)
     for _ in range(args.warmup):
-        cpu_reference_sample(args, sol.rates, 1, warmup=0)
-    tps, dt, desc, threads = cpu_reference_sample(args, sol.rates, args.steps, warmup=0)
+        cpu_reference_sample(args, rates, 1, warmup=0)
+    tps, dt, desc, threads = cpu_reference_sample(args, rates, args.steps, warmup=0)
     line = {
-        "impl": "reference", "metric": METRIC, "value": tps, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_name(args), "value": tps, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "mixtral-8x7b-moe-ffn-decode", "batch": args.batch, "model_dim": args.model_dim,
-                   "hidden_dim": args.hidden_dim, "experts": args.experts, "top_k": args.top_k,
-                   "rates": {"cc": sol.rates.cc, "cg": sol.rates.cg, "gg": sol.rates.gg}},
+        "config": base_config(args, rates, args.batch, 1),
         "cpu_baseline": {"value": tps, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
         "e2e": {"value": tps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    del per_step
     print(json.dumps(line), flush=True)
 
 
-def make_experts(args, rates, rank, world, device):
-    """Random-init bf16 Mixtral experts (HF layout), placed by `rates`; rank r
-    owns experts e with e % world == r."""
+def make_experts(args, rates, owned, device):
+    """Random-init experts (HF layout) placed by `rates`."""
     import torch
 
     from paper_2411_15715_b200.sliced import SlicedFFN
 
     M, H = args.model_dim, args.hidden_dim
+    tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     experts = {}
-    for e in range(args.experts):
-        if e % world != rank:
-            continue
+    for e in owned:
         g = torch.Generator(device=device).manual_seed(1000 + e)
-        w1t = (torch.randn(H, M, device=device, generator=g) / 64).to(torch.bfloat16).cpu()
-        w3t = (torch.randn(H, M, device=device, generator=g) / 64).to(torch.bfloat16).cpu()
-        w2t = (torch.randn(M, H, device=device, generator=g) / 120).to(torch.bfloat16).cpu()
-        experts[e] = SlicedFFN(w1t, w2t, rates, w3t=w3t, activation="silu", dtype="bf16", device=device.index)
+        w1t = (torch.randn(H, M, device=device, generator=g) / 64).to(tdt).cpu()
+        w3t = (torch.randn(H, M, device=device, generator=g) / 64).to(tdt).cpu()
+        w2t = (torch.randn(M, H, device=device, generator=g) / 120).to(tdt).cpu()
+        experts[e] = SlicedFFN(w1t, w2t, rates, w3t=w3t, activation="silu", dtype=args.dtype, device=device.index)
         del w1t, w3t, w2t
     return experts
-
-
-def routed_calls(experts, router, x_host, top_k):
-    from paper_2411_15715_b200.sliced import CallSpec, route_topk
-
-    ids, gates = route_topk(x_host.astype(np.float64) @ router, top_k)
-    calls = []
-    for e, ffn in experts.items():
-        rows, slots = np.nonzero(ids == e)
-        if rows.size:
-            calls.append(CallSpec(ffn.layer, rows.astype(np.int32), gates[rows, slots].astype(np.float32)))
-    return calls
 
 
 def run_ours(args):
     import torch
 
     from paper_2411_15715_b200 import _native as nat
-    from paper_2411_15715_b200.sliced import forward_calls
+    from paper_2411_15715_b200.expert_parallel import ExpertParallelMoE, local_experts
 
     world, rank, local = dist_env()
     device = torch.device("cuda", local)
@@ -260,39 +264,26 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=device)
         os.environ.setdefault("SP_HOST_THREADS", str(max(1, (os.cpu_count() or 16) // world)))
+        dist.init_process_group("nccl", device_id=device)
     nat.init(local)
 
     B = args.batch
     global_batch = B * world
-    sol, layer, budget, source, profile = plan_rates(args, B)
-    rates = sol.rates
-    experts = make_experts(args, rates, rank, world, device)
+    rates, budget, source, profile = plan_rates(args, B)
+    experts = make_experts(args, rates, local_experts(args.experts, rank, world), device)
     rng = np.random.default_rng(7)
     router = rng.standard_normal((args.model_dim, args.experts))
+    moe = ExpertParallelMoE(experts, router, args.top_k, args.experts, out_dim=args.model_dim)
     pool = 64
-    xs_host = [rng.standard_normal((global_batch, args.model_dim)).astype(np.float32) for _ in range(pool)]
-    xs_dev = [torch.from_numpy(x).to(device, torch.bfloat16) for x in xs_host]
-    xs_host_bf = [x.float().cpu().numpy() for x in xs_dev]  # routing sees the bf16 values
-    plans = [routed_calls(experts, router, xh, args.top_k) for xh in xs_host_bf]
-    out = torch.empty(global_batch, args.model_dim, device=device, dtype=torch.bfloat16)
+    tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    xs_dev = [torch.from_numpy(rng.standard_normal((global_batch, args.model_dim)).astype(np.float32)).to(device, tdt)
+              for _ in range(pool)]
+    xs_host = [x.float().cpu().numpy() for x in xs_dev]  # routing sees the values the kernels see
 
     def step(i, host_io=False):
-        calls = plans[i % pool]
-        if host_io:
-            if calls:
-                y = forward_calls(calls, xs_host_bf[i % pool])
-            else:
-                y = np.zeros((global_batch, args.model_dim), dtype=np.float32)
-            return y
-        if calls:
-            forward_calls(calls, xs_dev[i % pool], out=out)
-        else:
-            out.zero_()
-        if dist is not None:
-            dist.all_reduce(out)
-        return out
+        j = i % pool
+        return moe(xs_host[j] if host_io else xs_dev[j], x_host=xs_host[j])
 
     def timed(n, host_io=False, trace=False):
         if dist is not None:
@@ -305,11 +296,7 @@ def run_ours(args):
         a.record()
         t0 = time.perf_counter()
         for i in range(n):
-            y = step(i, host_io)
-            if host_io and dist is not None:
-                yt = torch.from_numpy(np.ascontiguousarray(y)).to(device)
-                dist.all_reduce(yt)
-                y = yt.cpu().numpy()
+            step(i, host_io)
         b.record()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -329,16 +316,20 @@ def run_ours(args):
         step(i, host_io=True)
     torch.cuda.synchronize()
 
-    with ClockSampler(local) as clk:
-        ms_step, wall_step, launches, spans = timed(args.steps, trace=True)
+    clk = ClockSampler(local).start()
+    clk.armed = True
+    ms_step, wall_step, launches, spans = timed(args.steps, trace=True)
+    clk.armed = False
+    clk.stop()
     clocks = clk.summary()
     e2e_ms, _, _, _ = timed(args.steps, host_io=True)
     value = global_batch / (ms_step * 1e-3)
     e2e_value = global_batch / (e2e_ms * 1e-3)
 
-    # ---- kernel-level roofline from the trace ----
+    # ---- kernel-level roofline from the trace (CUDA events on the library's compute stream) ----
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"
     gg = [s for s in spans if s["kind"] == "gg"]
     cp = [s for s in spans if s["kind"] == "copy"]
     cc = [s for s in spans if s["kind"] == "cc"]
@@ -354,7 +345,7 @@ def run_ours(args):
     t_roof = max(gg_step_bytes / (hbm_peak * 1e9), cg_step_bytes / (link_peak * 1e9))
     cc_busy = sum(s["end_s"] - s["start_s"] for s in cc) / args.steps
     if args.trace_out and rank == 0:
-        Path(args.trace_out).write_text(json.dumps([s for s in spans if s["call"] < 3], indent=0))
+        Path(args.trace_out).write_text(json.dumps([s for s in spans if s["call"] < 4], indent=0))
 
     if rank != 0:
         if dist is not None:
@@ -367,27 +358,26 @@ def run_ours(args):
         tps, dt, desc, threads = cpu_reference_sample(args, rates, args.cpu_sample_steps)
         cpu = {"value": tps, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
 
-    widths = next(iter(experts.values())).block_widths if experts else None
-    placed = next(iter(experts.values())).layer.placed_bytes() if experts else {}
+    first = next(iter(experts.values())) if experts else None
+    xel = 2 if args.dtype == "bf16" else 4
+    config = base_config(args, rates, global_batch, world)
+    config.update({
+        "block_widths": first.block_widths if first else None,
+        "gpu_budget_bytes": budget, "budget_frac": args.budget_frac, "profile": source,
+        "placed_bytes_per_expert": first.layer.placed_bytes() if first else {},
+        "l2": "inputs larger than L2: 8 experts' GG blocks (>1 GB) rotate with routing",
+    })
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric_name(args), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init bf16 weights, seeded)",
-        "config": {
-            "workload": "mixtral-8x7b-moe-ffn-decode", "model_dim": args.model_dim, "hidden_dim": args.hidden_dim,
-            "experts": args.experts, "top_k": args.top_k, "batch_per_gpu": B, "global_batch": global_batch,
-            "parallelism": f"ep{world}" if world > 1 else "single",
-            "rates": {"cc": rates.cc, "cg": rates.cg, "gg": rates.gg}, "block_widths": widths,
-            "gpu_budget_bytes": budget, "budget_frac": args.budget_frac, "profile": source,
-            "placed_bytes_per_expert": placed,
-            "l2": "inputs larger than L2: 8 experts x GG block rotate with routing (>1 GB per pass)",
-        },
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": global_batch * args.model_dim * 2,
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (random-init weights, seeded)",
+        "config": config,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": global_batch * args.model_dim * xel,
                 "d2h_bytes_per_step": global_batch * args.model_dim * 4},
-        "roofline": {"bound": "hbm", "kernel": "GG GEMV pair (up+gate fused SwiGLU, down) per expert",
-                     "achieved": gg_gbs, "peak": hbm_peak, "unit": "GB/s",
+        "roofline": {"bound": "hbm", "kernel": "ffn_block_kernel on the GG block (fused up+gate+down, TMA bulk ring)",
+                     "achieved": gg_gbs, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": gg_gbs / hbm_peak if hbm_peak else None, "traffic": None,
-                     "algorithmic_bytes_per_launch_pair": gg_bytes, "mean_pair_us": gg_dt * 1e6},
+                     "algorithmic_bytes_per_launch": gg_bytes, "mean_launch_us": gg_dt * 1e6},
         "link": {"cg_copy_GBps_while_busy": cp_bytes / cp_busy / 1e9 if cp_busy else None,
                  "cg_GBps_over_step": cg_step_bytes / step_s / 1e9, "link_peak_GBps": link_peak,
                  "frac_over_step": (cg_step_bytes / step_s / 1e9) / link_peak if link_peak else None,

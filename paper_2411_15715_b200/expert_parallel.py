@@ -1,0 +1,112 @@
+"""Expert-parallel sliced MoE layer across GPUs (one process per GPU).
+
+SURVEY.md §8(e): experts shard naturally.  Rank r owns experts
+``e % world == r``; each owned expert keeps its own CC / CG / GG split, so every
+GPU streams its CG blocks over its own host link and runs its CC blocks on its
+share of the host cores.  All ranks route the same tokens (the router is tiny
+and replicated), compute their local experts' gated contributions with one
+``sp_forward_batch``, and one all-reduce (NCCL over NVLink on GPUs; gloo in the
+CPU tests) sums the partial outputs -- the path's only exchange step, since a
+token's output needs both of its top-2 experts.
+
+The local executor is pluggable (``local_forward``) so the sharding, routing
+and reduction logic can be exercised on CPU with world size 2; on GPUs it is
+``sliced.forward_calls``.
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Mapping, Sequence
+
+import numpy as np
+
+from .errors import ShapeMismatch
+from .sliced import CallSpec, forward_calls, route_topk
+
+
+def owner_of(expert: int, world: int) -> int:
+    """Round-robin expert placement."""
+    return expert % world
+
+
+def local_experts(n_experts: int, rank: int, world: int) -> list[int]:
+    return [e for e in range(n_experts) if owner_of(e, world) == rank]
+
+
+def route_local(x_host: np.ndarray, router_w: np.ndarray, top_k: int, owned: Sequence[int]):
+    """Top-k routing of every token (fp64, ties -> lower expert id), restricted
+    to the owned experts: [(expert, token_rows int32, gates float32)]."""
+    ids, gates = route_topk(np.asarray(x_host, dtype=np.float64) @ router_w, top_k)
+    plan = []
+    for e in owned:
+        rows, slots = np.nonzero(ids == e)
+        if rows.size:
+            order = np.argsort(rows, kind="stable")
+            rows, slots = rows[order], slots[order]
+            plan.append((e, rows.astype(np.int32), gates[rows, slots].astype(np.float32)))
+    return plan
+
+
+class ExpertParallelMoE:
+    """Top-k MoE whose experts are split over the ranks of a process group.
+
+    ``experts`` maps the expert ids this rank owns to placed layers
+    (``SlicedFFN``); ``local_forward(plan, x) -> y`` overrides the executor
+    (default: one ``sp_forward_batch`` over the owned, active experts).
+    """
+
+    def __init__(self, experts: Mapping[int, object], router_w, top_k: int, n_experts: int,
+                 group=None, local_forward: Callable | None = None, out_dim: int | None = None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.router_w = np.asarray(router_w, dtype=np.float64)
+        if self.router_w.shape[1] != n_experts:
+            raise ShapeMismatch("router_w must have one column per expert")
+        self.top_k = int(top_k)
+        self.n_experts = int(n_experts)
+        self.owned = local_experts(n_experts, self.rank, self.world)
+        missing = set(self.owned) - set(experts)
+        if missing:
+            raise ValueError(f"rank {self.rank} owns experts {sorted(missing)} but got no layer for them")
+        self.experts = dict(experts)
+        if out_dim is None:
+            out_dim = (next(iter(self.experts.values())).layer.out_dim if self.experts
+                       else self.router_w.shape[0])
+        self.out_dim = int(out_dim)
+        self.local_forward = local_forward or self._gpu_local_forward
+
+    def _gpu_local_forward(self, plan, x):
+        calls = [CallSpec(self.experts[e].layer, rows, gates) for e, rows, gates in plan]
+        return forward_calls(calls, x)
+
+    def forward(self, x, x_host: np.ndarray | None = None):
+        """y = sum over ranks of the owned experts' gated outputs (all-reduced).
+
+        ``x``: torch tensor [T, M] (CUDA for the GPU executor); ``x_host``: its
+        values on the host for routing (computed from ``x`` if omitted)."""
+        import torch
+
+        if x_host is None:
+            x_host = x.detach().float().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+        plan = route_local(x_host, self.router_w, self.top_k, self.owned)
+        if plan:
+            y = self.local_forward(plan, x)
+            if not isinstance(y, torch.Tensor):
+                y = torch.as_tensor(np.ascontiguousarray(y))
+        else:
+            dev = x.device if isinstance(x, torch.Tensor) else "cpu"
+            dt = x.dtype if isinstance(x, torch.Tensor) else torch.float64
+            y = torch.zeros((x_host.shape[0], self.out_dim), dtype=dt, device=dev)
+        if self.world > 1:
+            if y.device.type == "cpu" and self.dist.get_backend(self.group) == "nccl":
+                yd = y.to(f"cuda:{torch.cuda.current_device()}")
+                self.dist.all_reduce(yd, group=self.group)
+                return yd.cpu()
+            self.dist.all_reduce(y, group=self.group)
+        return y
+
+    __call__ = forward
