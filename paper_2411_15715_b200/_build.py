@@ -16,7 +16,7 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_native"
 LIB = OUT_DIR / "libsliced.so"
 SOURCES = ["runtime.cu", "host_cc.cpp"]
-HEADERS = ["kernels.cuh", "host_cc.h", "../../include/sliced.h"]
+HEADERS = ["kernels.cuh", "gemm_tc.cuh", "host_cc.h", "../../include/sliced.h"]
 
 NVCC_FLAGS = [
     "-O3",

@@ -28,6 +28,8 @@
 #include "../../include/sliced.h"
 #include "host_cc.h"
 #include "kernels.cuh"
+#include "gemm_tc.cuh"
+#include <cudaTypedefs.h>
 
 
 namespace sp {
@@ -383,14 +385,117 @@ struct BlockView {
 struct CallWs {
   float* part;     // [S][T_e][N] partial slices of every block of the call
   int S;           // slices in use
+  int tc_slice = -1;            // slice the tensor-core blocks accumulate into
+  __nv_bfloat16* x_tc = nullptr;  // [T_e, ldm] gathered bf16 x (tensor-core path)
+  __nv_bfloat16* a_tc = nullptr;  // [T_e, ld_a] bf16 hidden activations of one block
+  int64_t ld_a = 0;
   float* ycc;      // [T_e, N] CC partial (from the host)
   int32_t* ids;    // device
   float* gates;    // device
 };
 
+// ---- tensor-core (tcgen05) block path for many tokens -------------------------
+static const int g_tc_min_tokens = env_int("SP_TC_MIN_T", 16);
+
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [outer, inner] matrix, 128B swizzle, zero OOB fill.
+static int make_tmap(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int64_t row_bytes,
+                     int box_inner, int box_outer) {
+  auto enc = tmap_encoder();
+  if (!enc) return fail(SP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+  cuuint64_t strides[1] = {cuuint64_t(row_bytes)};
+  cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (res != CUDA_SUCCESS)
+    return fail(SP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): inner %lld outer %lld stride %lld", int(res),
+                (long long)inner, (long long)outer, (long long)row_bytes);
+  return SP_OK;
+}
+
+template <int BN, int NB>
+static int launch_gemm(Context* C, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
+                       tc::GemmArgs g, cudaStream_t s) {
+  auto kern = tc::gemm_kernel<BN, NB>;
+  constexpr int STAGE = tc::BM * tc::BK * 2 + NB * BN * tc::BK * 2;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+    attr_set = true;
+  }
+  g.stages = std::min(6, (kSmemLimit - 1024 - 256) / STAGE);
+  const size_t smem = size_t(g.stages) * STAGE + 1024 + 256;
+  dim3 grid(unsigned((g.n_valid + BN - 1) / BN), unsigned((g.m_valid + tc::BM - 1) / tc::BM));
+  kern<<<grid, tc::kThreads, smem, s>>>(a, b0, b1, g);
+  SP_CUDA(cudaGetLastError());
+  ++C->launches;
+  return SP_OK;
+}
+
+// up GEMM (fused SwiGLU / act) into a_tc, then down GEMM accumulated into the call's tc slice
+static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype, int64_t ldx,
+                        CallWs& w, const int32_t* dev_ids, int64_t T_e, int t0, int T, cudaStream_t s) {
+  const int64_t M = L->d.model_dim, N = L->d.out_dim, R = b.rows;
+  if (w.tc_slice < 0) {
+    w.tc_slice = w.S++;
+    SP_CUDA(cudaMemsetAsync(w.part + size_t(w.tc_slice) * T_e * N, 0, size_t(T_e) * N * 4, s));
+  }
+  // gathered bf16 x rows [T, M]
+  {
+    dim3 grid(unsigned(std::min<int64_t>((M + 255) / 256, 16)), unsigned(T));
+    tc::gather_rows_bf16_kernel<<<grid, 256, 0, s>>>(x, xdtype, ldx, dev_ids, t0, T, int(M), w.x_tc, L->ldm);
+    SP_CUDA(cudaGetLastError());
+    ++C->launches;
+  }
+  CUtensorMap tx, tw1, tw3, ta, tw2;
+  SP_TRY(make_tmap(&tx, w.x_tc, M, T, L->ldm * 2, tc::BK, tc::BM));
+  SP_TRY(make_tmap(&tw1, b.base, M, R, L->ldm * 2, tc::BK, 64));
+  SP_TRY(make_tmap(&tw3, L->d.gated ? b.base + b.w3_off : b.base, M, R, L->ldm * 2, tc::BK, 64));
+  tc::GemmArgs up{};
+  up.m_valid = T;
+  up.n_valid = int(R);
+  up.k = int(M);
+  up.mode = L->d.gated ? tc::kUpGated : tc::kUpPlain;
+  up.act = L->d.act;
+  up.a_out = w.a_tc;
+  up.lda = w.ld_a;
+  up.a_col0 = 0;
+  if (L->d.gated)
+    SP_TRY((launch_gemm<64, 2>(C, tx, tw1, tw3, up, s)));
+  else
+    SP_TRY((launch_gemm<64, 1>(C, tx, tw1, tw1, up, s)));
+  SP_TRY(make_tmap(&ta, w.a_tc, R, T, w.ld_a * 2, tc::BK, tc::BM));
+  SP_TRY(make_tmap(&tw2, b.base + b.w2_off, N, R, L->ldn * 2, 64, tc::BK));
+  tc::GemmArgs dn{};
+  dn.m_valid = T;
+  dn.n_valid = int(N);
+  dn.k = int(R);
+  dn.mode = tc::kDownAcc;
+  dn.y = w.part + size_t(w.tc_slice) * T_e * N + size_t(t0) * N;
+  dn.ldy = N;
+  dn.accumulate = 1;
+  return launch_gemm<64, 1>(C, ta, tw2, tw2, dn, s);
+}
+
 static int run_block(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,
                      int64_t ldx, CallWs& w, const int32_t* host_ids, int64_t T_e, int t0, int T,
                      cudaStream_t s) {
+  if (L->d.wdtype == SP_BF16 && T >= g_tc_min_tokens && w.x_tc && w.a_tc)
+    return run_block_tc(C, L, b, x, xdtype, ldx, w, w.ids, T_e, t0, T, s);
   const int grid = block_grid(C, b.rows);
   const int tt_max = max_token_tile(L->d.model_dim);
   if (tt_max == 0) return fail(SP_ERR_VALUE, "model_dim %lld exceeds the x tile", (long long)L->d.model_dim);
@@ -607,15 +712,23 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     dev_off += size_t(round_up(int64_t(bytes), 256));
     return o;
   };
-  std::vector<size_t> o_part(n_calls), o_ycc(n_calls), o_ids(n_calls), o_g(n_calls);
+  std::vector<size_t> o_part(n_calls), o_ycc(n_calls), o_ids(n_calls), o_g(n_calls), o_xtc(n_calls),
+      o_atc(n_calls);
+  std::vector<int64_t> ws_ld_a(n_calls);
   int64_t total_rows = 0;
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int64_t Te = calls[c].tokens;
-    int64_t slices = block_grid(C, L->h_gg);
+    int64_t slices = block_grid(C, L->h_gg) + 1;  // + the tensor-core accumulation slice
     for (int ci = 0; ci < int(L->chunks.size()); ++ci)
       if (ci >= L->n_cc_chunks || calls[c].n_g > 0) slices += block_grid(C, L->chunks[ci].rc);
-    o_part[c] = dalloc(size_t(std::max<int64_t>(slices, 1)) * Te * N * 4);
+    o_part[c] = dalloc(size_t(slices) * Te * N * 4);
+    const bool tc = L->d.wdtype == SP_BF16 && Te >= g_tc_min_tokens;
+    int64_t max_rows = L->h_gg;
+    for (const Chunk& ch : L->chunks) max_rows = std::max(max_rows, ch.rc);
+    ws_ld_a[c] = round_up(std::max<int64_t>(max_rows, 1), 64);
+    o_xtc[c] = tc ? dalloc(size_t(Te) * L->ldm * 2) : SIZE_MAX;
+    o_atc[c] = tc ? dalloc(size_t(Te) * ws_ld_a[c] * 2) : SIZE_MAX;
     o_ycc[c] = dalloc(size_t(Te) * N * 4);
     o_ids[c] = dalloc(size_t(Te) * 4);
     o_g[c] = dalloc(size_t(Te) * 4);
@@ -629,6 +742,11 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   for (int c = 0; c < n_calls; ++c) {
     ws[c].part = reinterpret_cast<float*>(dws + o_part[c]);
     ws[c].S = 0;
+    ws[c].ld_a = ws_ld_a[c];
+    if (o_xtc[c] != SIZE_MAX) {
+      ws[c].x_tc = reinterpret_cast<__nv_bfloat16*>(dws + o_xtc[c]);
+      ws[c].a_tc = reinterpret_cast<__nv_bfloat16*>(dws + o_atc[c]);
+    }
     ws[c].ycc = reinterpret_cast<float*>(dws + o_ycc[c]);
     ws[c].ids = reinterpret_cast<int32_t*>(dws + o_ids[c]);
     ws[c].gates = reinterpret_cast<float*>(dws + o_g[c]);

@@ -178,3 +178,41 @@ def test_full_size_mixtral_expert_bf16(sp, torch):
     assert orc.max_rel_error(y, ref) <= BF16_TOL
     # output rounding to bf16 dominates; the fp32 accumulation itself is much tighter
     assert orc.max_rel_error(y, ref) <= 5e-3
+
+
+@pytest.mark.parametrize("gated", [True, False])
+@pytest.mark.parametrize("T", [16, 64, 200])
+def test_prefill_tensor_core_path(sp, torch, gated, T):
+    """T >= 16 bf16 tokens go through the tcgen05 GEMM pair (up + fused SwiGLU,
+    down accumulate); CG chunks, the n_g diverted rows and the CC host rows
+    included."""
+    from paper_2411_15715_b200.sliced import SlicedFFN
+
+    rng = np.random.default_rng(100 + T + gated)
+    M, H = 512, 1664
+    w1t, w3t, w2t = (rng.standard_normal(s).astype(np.float32) / 16 for s in ((H, M), (H, M), (M, H)))
+    q = orc.bf16_round
+    for cc, cg, ng in ((0.0, 0.0, 0), (0.25, 0.25, 0), (0.25, 0.25, T // 2), (0.5, 0.0, T)):
+        ffn = SlicedFFN(w1t, w2t, sp.SlicingRates(cc, cg, 1.0 - cc - cg), w3t=w3t if gated else None,
+                        activation="silu", dtype="bf16", chunk_rows=256)
+        x = torch.from_numpy(rng.standard_normal((T, M)).astype(np.float32)).cuda().to(torch.bfloat16)
+        y = ffn(x, n_g=ng).float().cpu().numpy()
+        ref = orc.dense_forward(q(x.float().cpu().numpy()), q(w1t.T), q(w2t.T), "silu", q(w3t.T) if gated else None)
+        assert orc.max_rel_error(y, ref) <= BF16_TOL, (cc, cg, ng)
+
+
+def test_prefill_moe_tensor_core_path(sp, torch):
+    from paper_2411_15715_b200.sliced import SlicedFFN, SlicedMoE
+
+    rng = np.random.default_rng(321)
+    E, M, H, T = 8, 256, 768, 96
+    ws = [tuple(rng.standard_normal(s).astype(np.float32) / 8 for s in ((H, M), (H, M), (M, H))) for _ in range(E)]
+    experts = [SlicedFFN(w1t, w2t, sp.SlicingRates(0.2, 0.3, 0.5), w3t=w3t, dtype="bf16", chunk_rows=128)
+               for w1t, w3t, w2t in ws]
+    router = rng.standard_normal((M, E))
+    x = rng.standard_normal((T, M)).astype(np.float32)
+    xq = orc.bf16_round(x)
+    got = SlicedMoE(experts, router, 2)(torch.from_numpy(x).cuda().to(torch.bfloat16)).float().cpu().numpy()
+    q = orc.bf16_round
+    ref = orc.moe_forward(xq, [(q(a.T), q(b.T), q(c.T)) for a, b, c in ws], router, 2)
+    assert orc.max_rel_error(got, ref) <= BF16_TOL
