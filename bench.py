@@ -52,7 +52,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--layers", type=int, default=32, help="cfg3: layers per forward")
+    ap.add_argument("--distinct-layers", type=int, default=8, help="cfg3: distinct weight sets cycled over the layers")
+    ap.add_argument("--prompt", type=int, default=512, help="cfg3: prompt tokens")
+    ap.add_argument("--decode-steps", type=int, default=128, help="cfg3: decode tokens after the prompt")
+    ap.add_argument("--prompt-profile", default=str(ROOT / "profiles" / "b200_prompt.json"))
     ap.add_argument("--batch", type=int, default=1, help="decode tokens per step per GPU")
     ap.add_argument("--budget-frac", type=float, default=0.5,
                     help="GPU budget as a fraction of each expert's bytes (planner units)")
@@ -65,12 +70,17 @@ def parse():
     args = ap.parse_args()
     if args.config == "cfg1":
         args.model_dim, args.hidden_dim, args.dtype = 1024, 3584, "f32"
+    elif args.config == "cfg3" and args.steps == 100:
+        args.steps = 2  # prefill repetitions
     else:
         args.model_dim, args.hidden_dim, args.dtype = 4096, 14336, "bf16"
     return args
 
 
 def metric_name(args):
+    if args.config == "cfg3":
+        return ("prefill tokens/s, Mixtral-8x7B 32-layer MoE FFN stack, 512-token prompt with the "
+                "token-assignment split (n_g from solve_ng), then 128 decode steps")
     if args.config == "cfg1":
         return "decode tokens/s, MoE FFN layer 1024/3584 (8 experts top-2) fp32, fixed CC/CG/GG 0.2/0.3/0.5"
     return "decode tokens/s, Mixtral-8x7B MoE FFN layer (4096/14336, 8 experts top-2), sliced CC/CG/GG"
@@ -394,8 +404,115 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_prefill_decode(args):
+    """BASELINE configs[2]: L MoE FFN layers, a P-token prompt routed top-2 per
+    layer, each expert's share T_e split by the token assigner (solve_ng on the
+    prompt-phase B200 profile, rates frozen from decode): the last n_g rows run
+    the CC columns on the GPU (streamed CC chunks), the rest on host threads;
+    then decode steps through the same layers."""
+    import torch
+
+    import paper_2411_15715_b200 as sp
+    from paper_2411_15715_b200 import _native as nat
+    from paper_2411_15715_b200.sliced import CallSpec, forward_calls, route_topk
+
+    world, rank, local = dist_env()
+    if world > 1:
+        raise SystemExit("cfg3 runs on one GPU")
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    nat.init(local)
+    rates, budget, source, _ = plan_rates(args, 1)
+    p_profile, p_source = load_profile(args.prompt_profile)
+    if p_source.startswith("fallback"):
+        p_profile, p_source = load_profile(args.profile)
+    layer_spec = sp.LayerSpec(args.model_dim, args.hidden_dim, n_gemms=3, precision=sp.Precision.FP16)
+    D = min(args.distinct_layers, args.layers)
+    sets = [make_experts(args, rates, range(args.experts), device) for _ in range(D)]
+    rng = np.random.default_rng(11)
+    routers = [rng.standard_normal((args.model_dim, args.experts)) for _ in range(D)]
+    xp = torch.from_numpy(rng.standard_normal((args.prompt, args.model_dim)).astype(np.float32)).to(device, torch.bfloat16)
+    xp_host = xp.float().cpu().numpy()
+    xd = [torch.from_numpy(rng.standard_normal((1, args.model_dim)).astype(np.float32)).to(device, torch.bfloat16)
+          for _ in range(16)]
+    xd_host = [x.float().cpu().numpy() for x in xd]
+    ng_cache: dict[int, int] = {}
+
+    def n_g_for(t_e: int) -> int:
+        if t_e not in ng_cache:
+            ng_cache[t_e] = sp.solve_ng(p_profile, layer_spec, t_e, rates).n_g
+        return ng_cache[t_e]
+
+    def plan(d, x_host, split):
+        ids, gates = route_topk(x_host.astype(np.float64) @ routers[d], args.top_k)
+        calls = []
+        for e, ffn in sets[d].items():
+            rows, slots = np.nonzero(ids == e)
+            if rows.size:
+                calls.append(CallSpec(ffn.layer, rows.astype(np.int32), gates[rows, slots].astype(np.float32),
+                                      n_g_for(rows.size) if split else 0))
+        return calls
+
+    prompt_plans = [plan(d, xp_host, True) for d in range(D)]
+    decode_plans = [[plan(d, xh, False) for xh in xd_host] for d in range(D)]
+    out_p = torch.empty_like(xp)
+    out_d = torch.empty_like(xd[0])
+
+    def prefill():
+        for l in range(args.layers):
+            forward_calls(prompt_plans[l % D], xp, out=out_p)
+
+    def decode():
+        for i in range(args.decode_steps):
+            for l in range(args.layers):
+                forward_calls(decode_plans[l % D][i % 16], xd[i % 16], out=out_d)
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) * 1e-3
+
+    for _ in range(max(1, args.warmup)):
+        prefill()
+    clk = ClockSampler(local).start()
+    clk.armed = True
+    l0 = nat.stats()["kernel_launches"]
+    t_p = min(timed(prefill) for _ in range(max(1, args.steps)))
+    t_d = timed(decode)
+    launches = nat.stats()["kernel_launches"] - l0
+    clk.armed = False
+    clk.stop()
+    ng_used = {t: n for t, n in sorted(ng_cache.items())}
+    t_e_prompt = sorted({len(c.token_ids) for c in prompt_plans[0]})
+    # host-I/O prefill through the public API
+    t_e2e = timed(lambda: [forward_calls(prompt_plans[l % D], xp_host) for l in range(args.layers)])
+    line = {
+        "metric": metric_name(args), "value": args.prompt / t_p, "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_p * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (random-init weights, seeded)",
+        "decode_tokens_per_s": args.decode_steps / t_d, "decode_ms_per_token": t_d / args.decode_steps * 1e3,
+        "config": {"workload": "mixtral-8x7b-32layer-prefill512-decode128", "layers": args.layers,
+                   "distinct_weight_sets": D, "prompt_tokens": args.prompt, "decode_steps": args.decode_steps,
+                   "model_dim": args.model_dim, "hidden_dim": args.hidden_dim, "experts": args.experts,
+                   "top_k": args.top_k, "rates": {"cc": rates.cc, "cg": rates.cg, "gg": rates.gg},
+                   "gpu_budget_frac": args.budget_frac, "decode_profile": source, "prompt_profile": p_source,
+                   "tokens_per_expert_layer0": t_e_prompt, "n_g_by_expert_tokens": ng_used,
+                   "l2": f"{D} distinct layers x 8 experts ({D * 2.8:.0f} GB) cycled, >> L2"},
+        "e2e": {"value": args.prompt / t_e2e, "unit": UNIT, "h2d_bytes_per_step": args.prompt * args.model_dim * 2 * args.layers,
+                "d2h_bytes_per_step": args.prompt * args.model_dim * 4 * args.layers},
+        "gpu_launches": launches, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.config == "cfg3" and args.impl == "ours":
+        return run_prefill_decode(args)
     if args.impl == "reference":
         run_reference(args)
     else:

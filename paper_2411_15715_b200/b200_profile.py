@@ -155,16 +155,20 @@ def launch_samples(torch, reps=20):
 
 
 def measure(phase: str = "decode", quick: bool = False) -> list[ProfileSample]:
+    """decode: T = 1 everywhere.  prompt: the GPU GEMM at T = 128 tokens (an
+    expert's share of a 512-token top-2 prompt, tensor-core path) and the host
+    GEMM at T = 32 -- one profile per phase, because t_G = alpha + T*M*H*beta
+    (pipeline.py:163) is linear in T while a GEMV/GEMM is not."""
     import torch
 
     nat.init(0)
-    tokens = 1 if phase == "decode" else 512
+    gpu_tokens, cpu_tokens = (1, 1) if phase == "decode" else (128, 32)
     widths = [256, 1024, 2048, 4096, 7168, 10240, 14336]
-    cpu_widths = [128, 256, 512, 1024, 2048, 4096]
+    cpu_widths = [128, 256, 512, 1024, 2048, 4096] if phase == "decode" else [64, 128, 256, 512]
     if quick:
-        widths, cpu_widths = [1024, 4096, 14336], [256, 1024, 2048]
-    samples = gpu_gemm_samples(torch, tokens, widths, reps=3 if quick else 5)
-    samples += cpu_gemm_samples(min(tokens, 8), cpu_widths, reps=2 if quick else 4)
+        widths, cpu_widths = [1024, 4096, 14336], cpu_widths[:3]
+    samples = gpu_gemm_samples(torch, gpu_tokens, widths, reps=3 if quick else 5)
+    samples += cpu_gemm_samples(cpu_tokens, cpu_widths, reps=2 if quick else 4)
     samples += c2g_samples(torch)
     samples += launch_samples(torch)
     return samples
@@ -173,7 +177,7 @@ def measure(phase: str = "decode", quick: bool = False) -> list[ProfileSample]:
 def main(argv=None) -> None:
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--out", default="profiles")
-    ap.add_argument("--phase", default="decode", choices=["decode"])
+    ap.add_argument("--phase", default="decode", choices=["decode", "prompt"])
     ap.add_argument("--quick", action="store_true")
     args = ap.parse_args(argv)
     out = Path(args.out)
