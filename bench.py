@@ -70,10 +70,10 @@ def parse():
     args = ap.parse_args()
     if args.config == "cfg1":
         args.model_dim, args.hidden_dim, args.dtype = 1024, 3584, "f32"
-    elif args.config == "cfg3" and args.steps == 100:
-        args.steps = 2  # prefill repetitions
     else:
         args.model_dim, args.hidden_dim, args.dtype = 4096, 14336, "bf16"
+    if args.config == "cfg3" and args.steps == 100:
+        args.steps = 2  # prefill repetitions
     return args
 
 
