@@ -178,10 +178,20 @@ struct FfnArgs {
   int kt;              // x tile: roundup(M, 256)
   int xvec;            // x rows 16-byte aligned and M a multiple of the 16-byte vector
   int tok[4];          // x rows of the launch's tokens (host-resolved ids), used when xvec
-  // partial slices: part[(slice0 + blockIdx.x) * slice_stride + (t0 + t) * N + n]
+  // partial slices: part[(slice0 + cta) * slice_stride + (t0 + t) * N + n]
   float* part;
   int64_t slice0, slice_stride;
   unsigned long long* stamps;  // debug timing: [grid][8] %globaltimer stamps, or null
+  int cta0, ncta;              // this block's CTAs inside a grouped launch
+};
+
+// Several blocks (e.g. the GG blocks of every active expert) in one launch:
+// CTAs [a[c].cta0, a[c].cta0 + a[c].ncta) work on entry c.  One launch, one
+// ramp and one tail per step instead of one per expert.
+constexpr int kMaxGroup = 8;
+struct FfnGroup {
+  FfnArgs a[kMaxGroup];
+  int n;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -204,7 +214,12 @@ struct FfnPlan {
 // smem: ring[NST][stage] | xs[TT][kt] | xraw[TT][M] (xvec) | part1[n_local][8][G][TT] |
 //       a_loc[n_local][TT] | full[NST] | empty[NST] | xbar
 template <typename WT, int TT, bool GATED, int NV>
-__global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, FfnPlan fp) {
+__global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __grid_constant__ FfnGroup grp,
+                                                                     const FfnPlan fp) {
+  int gi = 0;
+  while (gi + 1 < grp.n && int(blockIdx.x) >= grp.a[gi + 1].cta0) ++gi;
+  const FfnArgs& p = grp.a[gi];
+  const int cta = int(blockIdx.x) - p.cta0, ncta = p.ncta;
   constexpr int VE = VecTraits<WT>::kElems;
   constexpr int G = GATED ? 2 : 1;
   constexpr int STEP = 32 * VE;
@@ -214,8 +229,8 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   SP_STAMP(0);
-  const int64_t r_begin = (int64_t)p.rows * blockIdx.x / gridDim.x;
-  const int64_t r_end = (int64_t)p.rows * (blockIdx.x + 1) / gridDim.x;
+  const int64_t r_begin = (int64_t)p.rows * cta / ncta;
+  const int64_t r_end = (int64_t)p.rows * (cta + 1) / ncta;
   const int n_local = int(r_end - r_begin);
   const int NST = fp.stages;
   const int n_up = (n_local + fp.rs_up - 1) / fp.rs_up;
@@ -443,7 +458,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(FfnArgs p, 
   }
   SP_STAMP(5);
   // write this CTA's partial slice (a CTA with no rows writes zeros)
-  float* out = p.part + (p.slice0 + blockIdx.x) * p.slice_stride;
+  float* out = p.part + (p.slice0 + cta) * p.slice_stride;
 #pragma unroll
   for (int t = 0; t < TT; ++t) {
     if (t >= p.T) break;

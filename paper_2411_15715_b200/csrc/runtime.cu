@@ -327,7 +327,7 @@ static int max_token_tile(int64_t M) {
 }
 
 template <typename WT, int TT, bool GATED, int NV>
-static int launch_ffn_t(Context* C, const FfnArgs& a, int grid, cudaStream_t s) {
+static int launch_ffn_t(Context* C, const FfnGroup& grp, int grid, cudaStream_t s) {
   constexpr int G = GATED ? 2 : 1;
   auto kern = ffn_block_kernel<WT, TT, GATED, NV>;
   static bool attr_set = false;
@@ -335,7 +335,9 @@ static int launch_ffn_t(Context* C, const FfnArgs& a, int grid, cudaStream_t s) 
     SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
     attr_set = true;
   }
-  const int per_cta = (a.rows + grid - 1) / grid;
+  const FfnArgs& a = grp.a[0];
+  int per_cta = 1;
+  for (int i = 0; i < grp.n; ++i) per_cta = std::max(per_cta, (grp.a[i].rows + grp.a[i].ncta - 1) / grp.a[i].ncta);
   const int64_t row1 = a.ldm * int64_t(sizeof(WT)), row2 = a.ldn * int64_t(sizeof(WT));
   int rs_up = int(std::max<int64_t>(1, g_stage_bytes / (G * row1)));
   int rs_dn = int(std::max<int64_t>(1, g_stage_bytes / row2));
@@ -346,32 +348,40 @@ static int launch_ffn_t(Context* C, const FfnArgs& a, int grid, cudaStream_t s) 
   const size_t fixed = size_t(TT) * a.kt * 4 + xraw + size_t(per_cta) * kConsumers * G * TT * 4 +
                        size_t((per_cta * TT + 1) & ~1) * 4 + (2 * kMaxStages + 1) * 8 + 128;
   if (fixed + 2 * stage > size_t(kSmemLimit))
-    return fail(SP_ERR_VALUE, "block of %d rows (M=%d, N=%d) does not fit shared memory", a.rows, a.M, a.N);
+    return fail(SP_ERR_VALUE, "block of %d rows/CTA (M=%d, N=%d) does not fit shared memory", per_cta, a.M, a.N);
   const int nst = int(std::min<size_t>(g_max_stages, (kSmemLimit - fixed) / stage));
   FfnPlan fp{rs_up, rs_dn, nst, int(stage)};
-  kern<<<grid, kBlockThreads, size_t(nst) * stage + fixed, s>>>(a, fp);
+  kern<<<grid, kBlockThreads, size_t(nst) * stage + fixed, s>>>(grp, fp);
   SP_CUDA(cudaGetLastError());
   ++C->launches;
   return SP_OK;
 }
 
 template <typename WT, int TT, bool GATED>
-static int launch_nv(Context* C, const FfnArgs& a, int grid, cudaStream_t s) {
+static int launch_nv(Context* C, const FfnGroup& g, int grid, cudaStream_t s) {
+  const FfnArgs& a = g.a[0];
   const int n_vec = (a.N + VecTraits<WT>::kElems - 1) / VecTraits<WT>::kElems;
   const int nv = (n_vec + kConsumers * 32 - 1) / (kConsumers * 32);
-  if (nv <= 1) return launch_ffn_t<WT, TT, GATED, 1>(C, a, grid, s);
-  if (nv <= 2) return launch_ffn_t<WT, TT, GATED, 2>(C, a, grid, s);
-  if (nv <= 4) return launch_ffn_t<WT, TT, GATED, 4>(C, a, grid, s);
+  if (nv <= 1) return launch_ffn_t<WT, TT, GATED, 1>(C, g, grid, s);
+  if (nv <= 2) return launch_ffn_t<WT, TT, GATED, 2>(C, g, grid, s);
+  if (nv <= 4) return launch_ffn_t<WT, TT, GATED, 4>(C, g, grid, s);
   return fail(SP_ERR_VALUE, "out_dim %d exceeds the kernel's %d column vectors per thread", a.N, kMaxVec);
 }
 
 template <typename WT, bool GATED>
-static int launch_tt(Context* C, int tt, const FfnArgs& a, int grid, cudaStream_t s) {
+static int launch_tt(Context* C, int tt, const FfnGroup& g, int grid, cudaStream_t s) {
   switch (tt) {
-    case 1: return launch_nv<WT, 1, GATED>(C, a, grid, s);
-    case 2: return launch_nv<WT, 2, GATED>(C, a, grid, s);
-    default: return launch_nv<WT, 4, GATED>(C, a, grid, s);
+    case 1: return launch_nv<WT, 1, GATED>(C, g, grid, s);
+    case 2: return launch_nv<WT, 2, GATED>(C, g, grid, s);
+    default: return launch_nv<WT, 4, GATED>(C, g, grid, s);
   }
+}
+
+static int launch_group(Context* C, const sp_layer* L, int tt, const FfnGroup& g, int grid, cudaStream_t s) {
+  if (L->d.wdtype == SP_BF16)
+    return L->d.gated ? launch_tt<__nv_bfloat16, true>(C, tt, g, grid, s)
+                      : launch_tt<__nv_bfloat16, false>(C, tt, g, grid, s);
+  return L->d.gated ? launch_tt<float, true>(C, tt, g, grid, s) : launch_tt<float, false>(C, tt, g, grid, s);
 }
 
 // One weight block applied to tokens [t0, t0 + T) of a call: partial slices
@@ -491,14 +501,8 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
   return launch_gemm<64, 1>(C, ta, tw2, tw2, dn, s);
 }
 
-static int run_block(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,
-                     int64_t ldx, CallWs& w, const int32_t* host_ids, int64_t T_e, int t0, int T,
-                     cudaStream_t s) {
-  if (L->d.wdtype == SP_BF16 && T >= g_tc_min_tokens && w.x_tc && w.a_tc)
-    return run_block_tc(C, L, b, x, xdtype, ldx, w, w.ids, T_e, t0, T, s);
-  const int grid = block_grid(C, b.rows);
-  const int tt_max = max_token_tile(L->d.model_dim);
-  if (tt_max == 0) return fail(SP_ERR_VALUE, "model_dim %lld exceeds the x tile", (long long)L->d.model_dim);
+static FfnArgs ffn_args(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,
+                        int64_t ldx, const CallWs& w, int64_t T_e) {
   FfnArgs a{};
   a.w1t = b.base;
   a.w3t = L->d.gated ? b.base + b.w3_off : nullptr;
@@ -514,32 +518,45 @@ static int run_block(Context* C, const sp_layer* L, const BlockView& b, const vo
   a.ids = w.ids;
   a.act = L->d.act;
   a.kt = int(round_up(L->d.model_dim, 256));
-  {
-    const int vx = xdtype == SP_BF16 ? 8 : 4;
-    const size_t esz_x = xdtype == SP_BF16 ? 2 : 4;
-    a.xvec = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (ldx % vx == 0) &&
-             ((size_t(ldx) * esz_x) % 16 == 0) && (L->d.model_dim % vx == 0);
-  }
+  const int vx = xdtype == SP_BF16 ? 8 : 4;
+  const size_t esz_x = xdtype == SP_BF16 ? 2 : 4;
+  a.xvec = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (ldx % vx == 0) &&
+           ((size_t(ldx) * esz_x) % 16 == 0) && (L->d.model_dim % vx == 0);
   a.part = w.part;
   a.stamps = C->stamps;
   a.slice0 = w.S;
   a.slice_stride = T_e * L->d.out_dim;
+  return a;
+}
+
+static void set_tokens(FfnArgs& a, const int32_t* host_ids, int64_t T_e, int t0, int n) {
+  a.t0 = t0;
+  a.T = n;
+  for (int t = 0; t < 4; ++t) {
+    const int64_t i = std::min<int64_t>(t0 + t, T_e - 1);
+    a.tok[t] = host_ids ? host_ids[i] : int32_t(i);
+  }
+}
+
+static int run_block(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,
+                     int64_t ldx, CallWs& w, const int32_t* host_ids, int64_t T_e, int t0, int T,
+                     cudaStream_t s) {
+  if (L->d.wdtype == SP_BF16 && T >= g_tc_min_tokens && w.x_tc && w.a_tc)
+    return run_block_tc(C, L, b, x, xdtype, ldx, w, w.ids, T_e, t0, T, s);
+  const int grid = block_grid(C, b.rows);
+  const int tt_max = max_token_tile(L->d.model_dim);
+  if (tt_max == 0) return fail(SP_ERR_VALUE, "model_dim %lld exceeds the x tile", (long long)L->d.model_dim);
+  FfnArgs a = ffn_args(C, L, b, x, xdtype, ldx, w, T_e);
+  a.cta0 = 0;
+  a.ncta = grid;
   for (int tb = 0; tb < T; tb += tt_max) {
     const int n = std::min(tt_max, T - tb);
     const int tt = n <= 1 ? 1 : n <= 2 ? 2 : 4;
-    a.t0 = t0 + tb;
-    a.T = n;
-    for (int t = 0; t < 4; ++t) {
-      const int64_t i = std::min<int64_t>(a.t0 + t, T_e - 1);
-      a.tok[t] = host_ids ? host_ids[i] : int32_t(i);
-    }
-    int st;
-    if (L->d.wdtype == SP_BF16)
-      st = L->d.gated ? launch_tt<__nv_bfloat16, true>(C, tt, a, grid, s)
-                      : launch_tt<__nv_bfloat16, false>(C, tt, a, grid, s);
-    else
-      st = L->d.gated ? launch_tt<float, true>(C, tt, a, grid, s) : launch_tt<float, false>(C, tt, a, grid, s);
-    SP_TRY(st);
+    set_tokens(a, host_ids, T_e, t0 + tb, n);
+    FfnGroup g{};
+    g.a[0] = a;
+    g.n = 1;
+    SP_TRY(launch_group(C, L, tt, g, grid, s));
   }
   w.S += grid;
   return SP_OK;
@@ -834,15 +851,57 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   };
   if (cc_async) cc_submit(C, cc_work);
 
-  // ---- GG blocks (HBM resident) ----
-  for (int c = 0; c < n_calls; ++c) {
-    const sp_layer* L = calls[c].layer;
-    const int Te = int(calls[c].tokens);
-    if (Te == 0 || L->h_gg <= 0) continue;
-    BlockView b{static_cast<const char*>(L->gg), L->gg_w3_off, L->gg_w2_off, L->h_gg};
-    GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, double(L->gg_bytes) * ((Te + 3) / 4));
-    SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, 0, Te, C->s_comp));
-    span.end();
+  // ---- GG blocks (HBM resident): the decode-size calls share one grouped launch ----
+  {
+    const int tt_max = max_token_tile(M);
+    std::vector<int> group;
+    for (int c = 0; c < n_calls; ++c) {
+      const sp_layer* L = calls[c].layer;
+      const int Te = int(calls[c].tokens);
+      if (Te == 0 || L->h_gg <= 0) continue;
+      const bool tc = L->d.wdtype == SP_BF16 && Te >= g_tc_min_tokens;
+      const sp_layer* L0 = group.empty() ? L : calls[group[0]].layer;
+      const bool same = L->d.wdtype == L0->d.wdtype && L->d.gated == L0->d.gated && L->d.act == L0->d.act;
+      if (!tc && Te <= tt_max && same && int(group.size()) < kMaxGroup) {
+        group.push_back(c);
+        continue;
+      }
+      BlockView b{static_cast<const char*>(L->gg), L->gg_w3_off, L->gg_w2_off, L->h_gg};
+      GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, double(L->gg_bytes) * ((Te + 3) / 4));
+      SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, 0, Te, C->s_comp));
+      span.end();
+    }
+    if (!group.empty()) {
+      // CTAs proportional to each block's rows, one wave over the SMs
+      int64_t rows_total = 0;
+      double bytes = 0;
+      int te_max = 1;
+      for (int c : group) {
+        rows_total += calls[c].layer->h_gg;
+        bytes += double(calls[c].layer->gg_bytes);
+        te_max = std::max(te_max, int(calls[c].tokens));
+      }
+      FfnGroup g{};
+      int cta = 0;
+      for (int c : group) {
+        const sp_layer* L = calls[c].layer;
+        const int Te = int(calls[c].tokens);
+        int nc = int(double(C->num_sms) * double(L->h_gg) / double(rows_total));
+        nc = std::max(1, std::min(nc, block_grid(C, L->h_gg)));
+        BlockView b{static_cast<const char*>(L->gg), L->gg_w3_off, L->gg_w2_off, L->h_gg};
+        FfnArgs a = ffn_args(C, L, b, x_dev, xdtype, M, ws[c], Te);
+        set_tokens(a, calls[c].token_ids, Te, 0, Te);
+        a.cta0 = cta;
+        a.ncta = nc;
+        g.a[g.n++] = a;
+        cta += nc;
+        ws[c].S += nc;
+      }
+      const int tt = te_max <= 1 ? 1 : te_max <= 2 ? 2 : 4;
+      GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, bytes);
+      SP_TRY(launch_group(C, calls[group[0]].layer, tt, g, cta, C->s_comp));
+      span.end();
+    }
   }
 
   // ---- CG chunks (and CC chunks for the n_g diverted rows) through the ring ----
