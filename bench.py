@@ -210,6 +210,15 @@ def cpu_reference_sample(args, rates, steps, warmup=1):
 # ---------------------------------------------------------------------------
 
 
+def ncu_traffic(args):
+    """dram__bytes_read.sum + dram__bytes_write.sum per GG launch from the
+    committed ncu --set full capture of this workload (profiles/ncu_traffic.json)."""
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    if not f.exists():
+        return None
+    return json.loads(f.read_text()).get(f"{args.config}_gg_launch_bytes")
+
+
 def dist_env():
     return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
             int(os.environ.get("LOCAL_RANK", "0")))
@@ -292,8 +301,9 @@ def run_ours(args):
     xs_host = [x.float().cpu().numpy() for x in xs_dev]  # routing sees the values the kernels see
 
     def step(i, host_io=False):
+        # device I/O: routing reads x back from the GPU inside the timed region
         j = i % pool
-        return moe(xs_host[j] if host_io else xs_dev[j], x_host=xs_host[j])
+        return moe(xs_host[j], x_host=xs_host[j]) if host_io else moe(xs_dev[j])
 
     def timed(n, host_io=False, trace=False):
         if dist is not None:
@@ -386,7 +396,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": global_batch * args.model_dim * 4},
         "roofline": {"bound": "hbm", "kernel": "ffn_block_kernel on the GG block (fused up+gate+down, TMA bulk ring)",
                      "achieved": gg_gbs, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": gg_gbs / hbm_peak if hbm_peak else None, "traffic": None,
+                     "frac": gg_gbs / hbm_peak if hbm_peak else None, "traffic": ncu_traffic(args),
                      "algorithmic_bytes_per_launch": gg_bytes, "mean_launch_us": gg_dt * 1e6},
         "link": {"cg_copy_GBps_while_busy": cp_bytes / cp_busy / 1e9 if cp_busy else None,
                  "cg_GBps_over_step": cg_step_bytes / step_s / 1e9, "link_peak_GBps": link_peak,
