@@ -311,10 +311,14 @@ static const int g_min_rows_per_cta = std::max(1, env_int("SP_MIN_ROWS", 4));
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxTileFloats = 16384;  // TT * roundup(M, 256) floats of x <= 64 KB
 
+// Streamed chunks hide under their own PCIe copy (~150 us for 8 MB), so they
+// run on fewer, fatter CTAs: fewer partial slices for finalize_kernel.
+static const int g_chunk_min_rows = std::max(1, env_int("SP_CHUNK_MIN_ROWS", 16));
+
 // CTAs a block of `rows` hidden units is split over (also its partial-slice count).
-static int block_grid(const Context* C, int64_t rows) {
+static int block_grid(const Context* C, int64_t rows, int min_rows = g_min_rows_per_cta) {
   if (rows <= 0) return 0;
-  const int64_t by_rows = (rows + g_min_rows_per_cta - 1) / g_min_rows_per_cta;
+  const int64_t by_rows = (rows + min_rows - 1) / min_rows;
   return int(std::max<int64_t>(1, std::min<int64_t>(C->num_sms, by_rows)));
 }
 
@@ -540,10 +544,10 @@ static void set_tokens(FfnArgs& a, const int32_t* host_ids, int64_t T_e, int t0,
 
 static int run_block(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,
                      int64_t ldx, CallWs& w, const int32_t* host_ids, int64_t T_e, int t0, int T,
-                     cudaStream_t s) {
+                     cudaStream_t s, int min_rows = g_min_rows_per_cta) {
   if (L->d.wdtype == SP_BF16 && T >= g_tc_min_tokens && w.x_tc && w.a_tc)
     return run_block_tc(C, L, b, x, xdtype, ldx, w, w.ids, T_e, t0, T, s);
-  const int grid = block_grid(C, b.rows);
+  const int grid = block_grid(C, b.rows, min_rows);
   const int tt_max = max_token_tile(L->d.model_dim);
   if (tt_max == 0) return fail(SP_ERR_VALUE, "model_dim %lld exceeds the x tile", (long long)L->d.model_dim);
   FfnArgs a = ffn_args(C, L, b, x, xdtype, ldx, w, T_e);
@@ -738,7 +742,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     const int64_t Te = calls[c].tokens;
     int64_t slices = block_grid(C, L->h_gg) + 1;  // + the tensor-core accumulation slice
     for (int ci = 0; ci < int(L->chunks.size()); ++ci)
-      if (ci >= L->n_cc_chunks || calls[c].n_g > 0) slices += block_grid(C, L->chunks[ci].rc);
+      if (ci >= L->n_cc_chunks || calls[c].n_g > 0) slices += block_grid(C, L->chunks[ci].rc, g_chunk_min_rows);
     o_part[c] = dalloc(size_t(slices) * Te * N * 4);
     const bool tc = L->d.wdtype == SP_BF16 && Te >= g_tc_min_tokens;
     int64_t max_rows = L->h_gg;
@@ -932,11 +936,12 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         // a cg_prime block writes only rows [t0, Te) of its slices; the reducer sums every row
         const size_t slice = size_t(Te) * N * 4;
         SP_CUDA(cudaMemsetAsync(ws[c].part + size_t(ws[c].S) * Te * N, 0,
-                                slice * block_grid(C, ch.rc), C->s_comp));
+                                slice * block_grid(C, ch.rc, g_chunk_min_rows), C->s_comp));
       }
       {
         GpuSpan span(C, C->s_comp, 2, is_cc ? SP_TRACE_CG_PRIME : SP_TRACE_CG, double(ch.bytes));
-        SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, t0, Te - t0, C->s_comp));
+        SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, t0, Te - t0, C->s_comp,
+                         g_chunk_min_rows));
         span.end();
       }
       SP_CUDA(cudaEventRecord(C->ev_free[slot], C->s_comp));
