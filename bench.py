@@ -303,7 +303,7 @@ def run_ours(args):
     def step(i, host_io=False):
         # device I/O: routing reads x back from the GPU inside the timed region
         j = i % pool
-        return moe(xs_host[j], x_host=xs_host[j]) if host_io else moe(xs_dev[j])
+        return moe(xs_host[j]) if host_io else moe(xs_dev[j])
 
     def timed(n, host_io=False, trace=False):
         if dist is not None:

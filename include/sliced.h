@@ -121,6 +121,21 @@ int sp_layer_widths(sp_layer_t layer, int64_t widths[3]);
 int sp_forward_batch(const sp_call* calls, int n_calls, const void* x, int xdtype, int64_t T,
                      void* y, int ydtype, unsigned flags, void* stream);
 
+/* ---- MoE layer (router + dispatch) -------- */
+/* Top-k routing on the host in fp64: logits[t, e] = sum_m x[t, m] * router[m, e],
+ * the k largest (ties -> lower expert id), softmax over those k logits.
+ * ids / gates: [T, k].  Host-only; the oracle's route_topk is the parity check. */
+int sp_moe_route(const float* router, int64_t model_dim, int n_experts, int top_k, const void* x,
+                 int xdtype, int64_t T, int32_t* ids, float* gates);
+/* One MoE FFN layer: route x (one device->host read of x serves the router
+ * and the CC blocks), then a single batched forward over the active experts.
+ * layers[e] == NULL marks an expert owned by another rank (expert parallel):
+ * its tokens contribute nothing here.  Same x / y / flags / stream contract as
+ * sp_forward_batch. */
+int sp_moe_forward(const sp_layer_t* layers, int n_experts, const float* router, int top_k,
+                   const void* x, int xdtype, int64_t T, void* y, int ydtype, unsigned flags,
+                   void* stream);
+
 /* Host-only CC block (no GPU): y_cc[T, N] (f32) = sum over cc columns.  Used by
  * the CPU test suite and the host-core micro-benchmarks of the profile refit. */
 int sp_cc_forward_host(sp_layer_t layer, const void* x, int xdtype, int64_t T, float* y_cc,

@@ -79,6 +79,10 @@ SIGNATURES = {
                                    C.c_void_p, C.c_int, C.c_uint, C.c_void_p]),
     "sp_cc_forward_host": (C.c_int, [_c_layer, C.c_void_p, C.c_int, C.c_int64,
                                      C.POINTER(C.c_float), C.c_int]),
+    "sp_moe_route": (C.c_int, [C.POINTER(C.c_float), C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                               C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_float)]),
+    "sp_moe_forward": (C.c_int, [C.POINTER(_c_layer), C.c_int, C.POINTER(C.c_float), C.c_int, C.c_void_p,
+                                 C.c_int, C.c_int64, C.c_void_p, C.c_int, C.c_uint, C.c_void_p]),
     "sp_trace_enable": (C.c_int, [C.c_int]),
     "sp_trace_fetch": (C.c_int, [C.POINTER(TraceRecord), C.POINTER(C.c_int)]),
     "sp_stats": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),

@@ -15,6 +15,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <condition_variable>
 #include <functional>
@@ -136,6 +137,7 @@ struct Context {
   int ring_next = 0;
   DevBuf ws;         // device workspace
   PinnedBuf hpin;    // pinned host staging (ids/gates, x, y_cc, y)
+  PinnedBuf xroute;  // x read back for the MoE router (and reused by the CC blocks)
   std::vector<float> hscratch;
   std::unique_ptr<ThreadPool> pool;
   int host_threads = 1;
@@ -684,7 +686,8 @@ static int cc_wait(Context* C) {
 // forward
 
 static int forward_batch(Context* C, const sp_call* calls, int n_calls, const void* x, int xdtype,
-                         int64_t T, void* y, int ydtype, unsigned flags, cudaStream_t user) {
+                         int64_t T, void* y, int ydtype, unsigned flags, cudaStream_t user,
+                         const void* x_host_ready = nullptr) {
   // ---- validate everything before enqueuing anything ----
   if (n_calls < 1 || n_calls > kMaxCalls)
     return fail(SP_ERR_VALUE, "n_calls must lie in [1, %d], got %d", kMaxCalls, n_calls);
@@ -824,6 +827,9 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
                             C->s_comp));
     x_dev = dws + o_xdev;
     x_host = x;
+  } else if (need_cc && x_host_ready) {
+    x_host = x_host_ready;  // already read back by the caller (sp_moe_forward)
+    SP_CUDA(cudaEventRecord(C->ev_x, C->s_comp));
   } else if (need_cc) {
     SP_CUDA(cudaMemcpyAsync(hp + p_x, x, size_t(T) * M * xel, cudaMemcpyDeviceToHost, C->s_comp));
     SP_CUDA(cudaEventRecord(C->ev_x, C->s_comp));
@@ -995,6 +1001,97 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   }
   if (C->trace.on) ++C->trace.call;
   return SP_OK;
+}
+
+
+
+// ---------------------------------------------------------------------------
+// MoE routing (host, fp64) and the one-call MoE layer
+
+static int moe_route(const float* router, int64_t M, int E, int k, const void* x, int xdtype, int64_t T,
+                     int32_t* ids, float* gates) {
+  if (E < 1 || k < 1 || k > E) return fail(SP_ERR_VALUE, "top_k must lie in [1, %d], got %d", E, k);
+  std::vector<double> logit(static_cast<size_t>(E), 0.0);
+  std::vector<int> order(static_cast<size_t>(E), 0);
+  for (int64_t t = 0; t < T; ++t) {
+    std::fill(logit.begin(), logit.end(), 0.0);
+    for (int64_t m = 0; m < M; ++m) {
+      double xv;
+      if (xdtype == SP_BF16) {
+        const uint32_t u = uint32_t(static_cast<const uint16_t*>(x)[t * M + m]) << 16;
+        float f;
+        memcpy(&f, &u, 4);
+        xv = f;
+      } else {
+        xv = static_cast<const float*>(x)[t * M + m];
+      }
+      const float* rrow = router + m * E;
+      for (int e = 0; e < E; ++e) logit[e] += xv * double(rrow[e]);
+    }
+    for (int e = 0; e < E; ++e) order[e] = e;
+    // k largest, ties to the lower expert id (a stable descending sort)
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return logit[a] > logit[b]; });
+    const double top = logit[order[0]];
+    double z = 0.0;
+    for (int j = 0; j < k; ++j) z += std::exp(logit[order[j]] - top);
+    for (int j = 0; j < k; ++j) {
+      ids[t * k + j] = order[j];
+      gates[t * k + j] = float(std::exp(logit[order[j]] - top) / z);
+    }
+  }
+  return SP_OK;
+}
+
+static int moe_forward(Context* C, const sp_layer_t* layers, int E, const float* router, int k, const void* x,
+                       int xdtype, int64_t T, void* y, int ydtype, unsigned flags, cudaStream_t user) {
+  if (!layers || !router || !x || !y) return fail(SP_ERR_VALUE, "NULL argument");
+  if (T < 1) return fail(SP_ERR_SHAPE, "input must have at least one row, got T=%lld", (long long)T);
+  const sp_layer* any = nullptr;
+  for (int e = 0; e < E; ++e)
+    if (layers[e]) any = layers[e];
+  if (!any) return fail(SP_ERR_VALUE, "sp_moe_forward: no expert layer on this rank");
+  const int64_t M = any->d.model_dim;
+  const size_t xel = xdtype == SP_BF16 ? 2 : 4;
+  const bool host_io = flags & SP_IO_HOST;
+  // one read of x serves the router and every CC block
+  const void* xh = x;
+  if (!host_io) {
+    SP_TRY(C->xroute.ensure(size_t(T) * M * xel));
+    SP_CUDA(cudaEventRecord(C->ev_user, user));
+    SP_CUDA(cudaStreamWaitEvent(C->s_aux, C->ev_user, 0));
+    SP_CUDA(cudaMemcpyAsync(C->xroute.p, x, size_t(T) * M * xel, cudaMemcpyDeviceToHost, C->s_aux));
+    SP_CUDA(cudaStreamSynchronize(C->s_aux));
+    xh = C->xroute.p;
+  }
+  std::vector<int32_t> ids(static_cast<size_t>(T * k));
+  std::vector<float> gates(static_cast<size_t>(T * k));
+  SP_TRY(moe_route(router, M, E, k, xh, xdtype, T, ids.data(), gates.data()));
+  // group token rows by expert (ascending token order per expert)
+  std::vector<std::vector<int32_t>> rows(static_cast<size_t>(E));
+  std::vector<std::vector<float>> g(static_cast<size_t>(E));
+  for (int64_t t = 0; t < T; ++t)
+    for (int j = 0; j < k; ++j) {
+      const int e = ids[t * k + j];
+      rows[e].push_back(int32_t(t));
+      g[e].push_back(gates[t * k + j]);
+    }
+  std::vector<sp_call> calls;
+  for (int e = 0; e < E; ++e)
+    if (layers[e] && !rows[e].empty())
+      calls.push_back(sp_call{layers[e], int64_t(rows[e].size()), rows[e].data(), g[e].data(), 0});
+  if (calls.empty()) {
+    // nothing routed to this rank's experts: y = 0
+    const size_t bytes = size_t(T) * any->d.out_dim * (ydtype == SP_BF16 ? 2 : 4);
+    if (host_io) {
+      memset(y, 0, bytes);
+      return SP_OK;
+    }
+    SP_CUDA(cudaMemsetAsync(y, 0, bytes, user));
+    return SP_OK;
+  }
+  if (int(calls.size()) > kMaxCalls) return fail(SP_ERR_VALUE, "%zu active experts exceed %d", calls.size(), kMaxCalls);
+  return forward_batch(C, calls.data(), int(calls.size()), x, xdtype, T, y, ydtype, flags, user,
+                       host_io ? nullptr : xh);
 }
 
 }  // namespace sp
@@ -1181,6 +1278,24 @@ int sp_forward_batch(const sp_call* calls, int n_calls, const void* x, int xdtyp
   std::lock_guard<std::mutex> g(C->mu);
   return forward_batch(C, calls, n_calls, x, xdtype, T, y, ydtype, flags,
                        static_cast<cudaStream_t>(stream));
+}
+
+int sp_moe_route(const float* router, int64_t model_dim, int n_experts, int top_k, const void* x,
+                 int xdtype, int64_t T, int32_t* ids, float* gates) {
+  if (!router || !x || !ids || !gates) return fail(SP_ERR_VALUE, "NULL argument");
+  if (model_dim < 1 || T < 0) return fail(SP_ERR_SHAPE, "bad router shape");
+  return moe_route(router, model_dim, n_experts, top_k, x, xdtype, T, ids, gates);
+}
+
+int sp_moe_forward(const sp_layer_t* layers, int n_experts, const float* router, int top_k, const void* x,
+                   int xdtype, int64_t T, void* y, int ydtype, unsigned flags, void* stream) {
+  Context* C = ctx_or_null();
+  if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  if (C->host_only)
+    return fail(SP_ERR_STATE, "host-only context: the GG/CG blocks need a CUDA device (no CPU fallback)");
+  std::lock_guard<std::mutex> g(C->mu);
+  return moe_forward(C, layers, n_experts, router, top_k, x, xdtype, T, y, ydtype, flags,
+                     static_cast<cudaStream_t>(stream));
 }
 
 int sp_cc_forward_host(sp_layer_t L, const void* x, int xdtype, int64_t T, float* y_cc,

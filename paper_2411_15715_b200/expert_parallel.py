@@ -21,7 +21,7 @@ from typing import Callable, Mapping, Sequence
 import numpy as np
 
 from .errors import ShapeMismatch
-from .sliced import CallSpec, forward_calls, route_topk
+from .sliced import CallSpec, forward_calls, moe_forward, route_topk
 
 
 def owner_of(expert: int, world: int) -> int:
@@ -90,6 +90,13 @@ class ExpertParallelMoE:
         values on the host for routing (computed from ``x`` if omitted)."""
         import torch
 
+        if x_host is None and self.local_forward == self._gpu_local_forward:
+            # native routing + dispatch: one read-back of x serves router and CC blocks
+            layers = [self.experts[e].layer if e in self.experts else None for e in range(self.n_experts)]
+            y = moe_forward(layers, self.router_w, self.top_k, x)
+            if not isinstance(y, torch.Tensor):
+                y = torch.as_tensor(np.ascontiguousarray(y))
+            return self._reduce(y)
         if x_host is None:
             x_host = x.detach().float().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
         plan = route_local(x_host, self.router_w, self.top_k, self.owned)
@@ -101,6 +108,12 @@ class ExpertParallelMoE:
             dev = x.device if isinstance(x, torch.Tensor) else "cpu"
             dt = x.dtype if isinstance(x, torch.Tensor) else torch.float64
             y = torch.zeros((x_host.shape[0], self.out_dim), dtype=dt, device=dev)
+        return self._reduce(y)
+
+    def _reduce(self, y):
+        """Sum the ranks' partial outputs (one all-reduce: NCCL on GPUs)."""
+        import torch
+
         if self.world > 1:
             if y.device.type == "cpu" and self.dist.get_backend(self.group) == "nccl":
                 yd = y.to(f"cuda:{torch.cuda.current_device()}")

@@ -494,6 +494,55 @@ def route_topk(logits: np.ndarray, k: int) -> tuple[np.ndarray, np.ndarray]:
     return ids, e / e.sum(axis=1, keepdims=True)
 
 
+def moe_route(x, router_w, top_k: int) -> tuple[np.ndarray, np.ndarray]:
+    """The runtime's router (libsliced sp_moe_route): fp64 logits x @ router_w,
+    top-k with ties to the lower expert id, softmax over the k logits."""
+    if getattr(x, "dtype", None) == np.uint16:  # bf16 bit patterns
+        xh, code = np.ascontiguousarray(x), nat.SP_BF16
+    else:
+        xh, code = np.ascontiguousarray(np.asarray(x), dtype=np.float32), nat.SP_F32
+    router = np.ascontiguousarray(router_w, dtype=np.float32)
+    T, M = xh.shape
+    ids = np.empty((T, top_k), dtype=np.int32)
+    gates = np.empty((T, top_k), dtype=np.float32)
+    nat.check(nat.lib().sp_moe_route(router.ctypes.data_as(C.POINTER(C.c_float)), M, router.shape[1], int(top_k),
+                                     xh.ctypes.data, code, T, ids.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     gates.ctypes.data_as(C.POINTER(C.c_float))))
+    return ids, gates
+
+
+def moe_forward(layers: Sequence["NativeLayer | None"], router_w, top_k: int, x, out=None):
+    """One MoE FFN layer in one native call (sp_moe_forward): route in the
+    runtime (the single read-back of x serves the router and the CC blocks),
+    then one batched forward over the active experts.  ``layers[e] is None``
+    marks an expert owned by another rank."""
+    torch = _maybe_torch()
+    router = np.ascontiguousarray(router_w, dtype=np.float32)
+    arr = (C.c_void_p * len(layers))(*[None if l is None else l.handle.value for l in layers])
+    first = next(l for l in layers if l is not None)
+    N = first.out_dim
+    rp = router.ctypes.data_as(C.POINTER(C.c_float))
+    if torch is not None and isinstance(x, torch.Tensor) and x.is_cuda:
+        x = x.contiguous()
+        if x.dtype not in (torch.bfloat16, torch.float32):
+            x = x.float()
+        xcode = nat.SP_BF16 if x.dtype == torch.bfloat16 else nat.SP_F32
+        if out is None:
+            out = torch.empty((x.shape[0], N), dtype=x.dtype, device=x.device)
+        ycode = nat.SP_BF16 if out.dtype == torch.bfloat16 else nat.SP_F32
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        nat.check(nat.lib().sp_moe_forward(arr, len(layers), rp, int(top_k), x.data_ptr(), xcode, x.shape[0],
+                                           out.data_ptr(), ycode, 0, C.c_void_p(stream)))
+        return out
+    if torch is not None and isinstance(x, torch.Tensor):
+        x = x.detach().float().numpy()
+    xh, xcode = _host_activations(x, first.dtype)
+    y = np.empty((xh.shape[0], N), dtype=np.float32) if out is None else out
+    nat.check(nat.lib().sp_moe_forward(arr, len(layers), rp, int(top_k), xh.ctypes.data, xcode, xh.shape[0],
+                                       y.ctypes.data, nat.SP_F32, nat.SP_IO_HOST, None))
+    return y
+
+
 class SlicedMoE:
     """Top-k MoE layer over SlicedFFN experts, each with its own CC/CG/GG split.
 
@@ -524,6 +573,9 @@ class SlicedMoE:
         return calls
 
     def forward(self, x, n_g: dict[int, int] | None = None, out=None):
+        if not n_g:
+            # routing + dispatch in the runtime: one native call per layer
+            return moe_forward([e.layer for e in self.experts], self.router_w, self.top_k, x, out)
         torch = _maybe_torch()
         if torch is not None and isinstance(x, torch.Tensor):
             x_host = x.detach().float().cpu().numpy()

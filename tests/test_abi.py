@@ -103,3 +103,24 @@ def test_cc_host_kernel_matches_oracle(host_ctx, dtype, gated, act):
         assert orc.max_rel_error(got, ref) <= 1e-5
         assert lay.block_widths == (H, 0, 0)
         assert lay.placed_bytes()["gg"] == 0 and lay.placed_bytes()["cc"] > 0
+
+
+def test_moe_router_matches_oracle():
+    """sp_moe_route (fp64 logits, top-k ties -> lower id, softmax over k) vs the oracle."""
+    from paper_2411_15715_b200.sliced import moe_route, to_bf16_bits
+
+    rng = np.random.default_rng(4)
+    for T, M, E, k in ((1, 4096, 8, 2), (7, 64, 16, 2), (5, 32, 8, 1), (3, 48, 4, 4)):
+        x = rng.standard_normal((T, M)).astype(np.float32)
+        router = rng.standard_normal((M, E)).astype(np.float32)
+        ids, gates = moe_route(x, router, k)
+        ref_ids, ref_g = orc.route_topk(x.astype(np.float64) @ router.astype(np.float64), k)
+        assert np.array_equal(ids, ref_ids)
+        np.testing.assert_allclose(gates, ref_g, rtol=1e-6)
+        xb = to_bf16_bits(x)
+        ids_b, _ = moe_route(xb, router, k)
+        ref_b, _ = orc.route_topk(orc.bf16_round(x) @ router.astype(np.float64), k)
+        assert np.array_equal(ids_b, ref_b)
+    # exact ties go to the lower expert id
+    ids, gates = moe_route(np.ones((1, 4), np.float32), np.ones((4, 6), np.float32), 2)
+    assert ids.tolist() == [[0, 1]] and np.allclose(gates, 0.5)
