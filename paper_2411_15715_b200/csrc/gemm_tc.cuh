@@ -1,22 +1,29 @@
-// gemm_tc.cuh -- tcgen05 / TMEM / TMA GEMM for the prefill (many-token) path, sm_100a.
+// gemm_tc.cuh -- tcgen05 / TMEM / TMA GEMMs for the prefill (many-token) path, sm_100a.
 //
-// Prefill is a real contraction: T tokens against every weight row, ~2*T
-// flop per weight byte.  Per block of hidden units (GG block or streamed chunk)
-// the path runs two GEMMs on the 5th-gen tensor cores:
-//   up   : a[T, R]  = act(x[T, M] . W1t[R, M]^T) * (x . W3t^T)     (SwiGLU epilogue, bf16 out)
-//   down : y[T, N] += a[T, R] . W2[R, N]                            (fp32 accumulate)
-// D[BM x BN] = A[BM x K] . B[BN x K]^T with A = tokens (UMMA M = 128), B = the
-// weights (K-major W1t/W3t rows for up, MN-major W2 rows for down), bf16
-// operands, fp32 accumulators in TMEM.
+// Prefill is a real contraction: T tokens against every weight row.  Per block
+// of hidden units (GG block or streamed chunk) the path runs two GEMMs on the
+// 5th-gen tensor cores, with the WEIGHTS as the 128-row UMMA M operand and the
+// tokens as N (<= 256), so each weight byte is streamed once per token tile:
+//   up   : D[h, t] = W1t[h, :] . x[t, :]  (and W3t)  -> a[t, h] = act(D1) * D3   (bf16)
+//   down : D[n, t] = W2[:, n] . a[t, :]               -> y[t, n] += D             (fp32)
+// A operands: W1t / W3t rows are K-major; W2 ([h, n], n contiguous) is MN-major.
+// B operands (x, a: [t, k] row-major) are K-major.  bf16 in, fp32 accumulate in TMEM.
 //
-// Warp roles (192 threads, one CTA per output tile):
+// Parallelism: a block has few 128-row tiles (56 for 7168 hidden units, 32
+// output-column tiles for N = 4096), so K is split over KS CTAs to put ~one CTA
+// on every SM.  Each split writes an fp32 partial tile; the LAST CTA of a tile
+// (atomic ticket) sums the KS partials in split order -- deterministic -- and
+// runs the epilogue (SwiGLU + bf16 store for up, accumulate into the call's
+// output slice for down), then re-arms the ticket.
+//
+// Warp roles (192 threads):
 //   warp 0      TMA producer: one lane issues cp.async.bulk.tensor 2D loads
-//               (128B swizzle) of A and B k-blocks into an S-deep smem ring
+//               (128B swizzle) into an S-deep smem ring
 //   warp 1      TMEM allocator + MMA issuer: one lane issues tcgen05.mma
-//               (kind::f16, cta_group::1, M=128, N=BN, K=16) and commits each
-//               stage back to the producer through an mbarrier
-//   warps 2..5  epilogue: tcgen05.ld 32x32b rows of the accumulator(s), fused
-//               activation / gate / accumulate, stores
+//               (kind::f16, cta_group::1, M = 128, N = NT, K = 16), commits
+//               stages back to the producer through mbarriers
+//   warps 2..5  epilogue: tcgen05.ld 32x32b (TMEM lane = weight row), fused
+//               epilogue or partial write + split fix-up
 #pragma once
 
 #include <cuda.h>
@@ -29,28 +36,30 @@
 namespace sp {
 namespace tc {
 
-constexpr int BM = 128;  // tokens per tile (UMMA M)
+constexpr int BM = 128;  // weight rows per tile (UMMA M)
 constexpr int BK = 64;   // k per stage: one 128-byte swizzle atom of bf16
 constexpr int UK = 16;   // UMMA K for 16-bit inputs
 constexpr int kThreads = 192;
 
-enum Mode : int { kUpGated = 0, kUpPlain = 1, kDownAcc = 2 };
+enum Mode : int { kUpGated = 0, kUpPlain = 1, kDown = 2 };
 
 struct GemmArgs {
-  int m_valid;      // valid token rows
-  int n_valid;      // valid B rows (hidden units for up, output columns for down)
-  int k;            // contraction length
   int mode;
   int act;
-  // up epilogue: a_out[(m0 + r) * lda + a_col0 + n]  (bf16)
+  int rows;         // weight rows (hidden units for up, output columns N for down)
+  int T;            // valid tokens
+  int k;            // contraction length
+  int m_tiles, t_tiles, ks;
+  int stages;
+  // up epilogue: a[t * lda + h]  (bf16)
   __nv_bfloat16* a_out;
   int64_t lda;
-  int64_t a_col0;
-  // down epilogue: y[(m0 + r) * ldy + n] (+)= acc  (fp32)
+  // down epilogue: y[t * ldy + n] += acc  (fp32, the call's tensor-core slice)
   float* y;
   int64_t ldy;
-  int accumulate;
-  int stages;
+  // split-K partials [tile][ks][NA][NT][128] fp32 and tickets [tile]
+  float* partial;
+  int* tickets;
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -72,12 +81,12 @@ __device__ __forceinline__ uint64_t umma_desc(const void* smem, uint32_t lbo_byt
   return d;
 }
 
-// kind::f16 instruction descriptor: bf16 x bf16 -> f32, A K-major.
-__host__ __device__ constexpr uint32_t umma_idesc(int m, int n, bool b_mn_major) {
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, B K-major.
+__host__ __device__ constexpr uint32_t umma_idesc(int m, int n, bool a_mn_major) {
   return (1u << 4)                          // D format f32
          | (1u << 7)                        // A format bf16
          | (1u << 10)                       // B format bf16
-         | (uint32_t(b_mn_major) << 16)     // B major
+         | (uint32_t(a_mn_major) << 15)     // A major
          | (uint32_t(n >> 3) << 17)         // N / 8
          | (uint32_t(m >> 4) << 24);        // M / 16
 }
@@ -104,27 +113,38 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BN, int NB>
+__device__ __forceinline__ void epilogue_sync() {
+  asm volatile("bar.sync 2, 128;" ::: "memory");
+}
+
+// NT: tokens per tile (UMMA N, multiple of 16, <= 256); NA: A operands (2 = W1t + W3t)
+template <int NT, int NA>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
-                const __grid_constant__ CUtensorMap tmB1, GemmArgs g) {
-  constexpr int A_BYTES = BM * BK * 2;
-  constexpr int B_BYTES = BN * BK * 2;
-  constexpr int STAGE = A_BYTES + NB * B_BYTES;
-  constexpr int TMEM_COLS = (NB * BN) <= 32 ? 32 : (NB * BN) <= 64 ? 64 : (NB * BN) <= 128 ? 128 : (NB * BN) <= 256 ? 256 : 512;
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
+                const __grid_constant__ CUtensorMap tmB, const GemmArgs g) {
+  constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+  constexpr int B_BYTES = NT * BK * 2;
+  constexpr int STAGE = NA * A_BYTES + B_BYTES;
+  constexpr int TMEM_COLS = (NA * NT) <= 32 ? 32 : (NA * NT) <= 64 ? 64 : (NA * NT) <= 128 ? 128
+                            : (NA * NT) <= 256 ? 256 : 512;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte alignment for the swizzled tiles
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = g.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(S) * STAGE);
   uint64_t* empty = full + S;
   uint64_t* tmem_full = empty + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  // blockIdx -> (token tile, row tile, split)
+  const int ks_id = blockIdx.x % g.ks;
+  const int tile = blockIdx.x / g.ks;  // = tt * m_tiles + mt
+  const int mt = tile % g.m_tiles, tt = tile / g.m_tiles;
+  const int m0 = mt * BM, t0 = tt * NT;
   const int nkb = (g.k + BK - 1) / BK;
-  const bool b_mn = g.mode == kDownAcc;
+  const int kb0 = nkb * ks_id / g.ks, kb1 = nkb * (ks_id + 1) / g.ks;
+  const bool a_mn = g.mode == kDown;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -133,8 +153,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(tmem_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB0)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA0)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -150,79 +170,123 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % S;
-        if (kb >= S) mbar_wait(&empty[s], ((kb / S) - 1) & 1);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int i = kb - kb0, s = i % S;
+        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
         unsigned char* st = smem + size_t(s) * STAGE;
         mbar_expect_tx(&full[s], STAGE);
-        tma_load_2d(st, &tmA, &full[s], kb * BK, m0);
-        if (!b_mn) {
-          tma_load_2d(st + A_BYTES, &tmB0, &full[s], kb * BK, n0);
-          if constexpr (NB == 2) tma_load_2d(st + A_BYTES + B_BYTES, &tmB1, &full[s], kb * BK, n0);
+        if (!a_mn) {
+          tma_load_2d(st, &tmA0, &full[s], kb * BK, m0);
+          if constexpr (NA == 2) tma_load_2d(st + A_BYTES, &tmA1, &full[s], kb * BK, m0);
         } else {
-          // MN-major B: boxes of 64 columns x BK rows, one per 64-column group
-#pragma unroll
-          for (int j = 0; j < BN / 64; ++j)
-            tma_load_2d(st + A_BYTES + j * (BK * 128), &tmB0, &full[s], n0 + j * 64, kb * BK);
+          // MN-major A (W2 [k rows][n]): two 64-column boxes of BK rows
+          tma_load_2d(st, &tmA0, &full[s], m0, kb * BK);
+          tma_load_2d(st + BK * 128, &tmA0, &full[s], m0 + 64, kb * BK);
         }
+        tma_load_2d(st + NA * A_BYTES, &tmB, &full[s], kb * BK, t0);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    const uint32_t idesc = umma_idesc(BM, BN, b_mn);
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % S;
-      mbar_wait(&full[s], (kb / S) & 1);
+    const uint32_t idesc = umma_idesc(BM, NT, a_mn);
+    for (int kb = kb0; kb < kb1; ++kb) {
+      const int i = kb - kb0, s = i % S;
+      mbar_wait(&full[s], (i / S) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (lane == 0) {
         const unsigned char* st = smem + size_t(s) * STAGE;
 #pragma unroll
         for (int kk = 0; kk < BK / UK; ++kk) {
-          const uint64_t a = umma_desc(st + kk * 32, 16, 1024);
+          const uint64_t b = umma_desc(st + NA * A_BYTES + kk * 32, 16, 1024);
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            const unsigned char* bt = st + A_BYTES + b * B_BYTES;
-            const uint64_t bd = b_mn ? umma_desc(bt + kk * UK * 128, BK * 128, 1024)  // k rows of 128 B
-                                     : umma_desc(bt + kk * 32, 16, 1024);
-            umma_bf16(tmem + uint32_t(b * BN), a, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          for (int a = 0; a < NA; ++a) {
+            const uint64_t ad = a_mn ? umma_desc(st + kk * UK * 128, BK * 128, 1024)
+                                     : umma_desc(st + a * A_BYTES + kk * 32, 16, 1024);
+            umma_bf16(tmem + uint32_t(a * NT), ad, b, idesc, (i > 0 || kk > 0) ? 1u : 0u);
           }
         }
         umma_commit(&empty[s]);
-        if (kb == nkb - 1) umma_commit(tmem_full);
+        if (kb == kb1 - 1) umma_commit(tmem_full);
       }
       __syncwarp();
     }
   } else {
-    // ---------------- epilogue: warps 2..5 cover TMEM lanes 32*(warp%4) ----------------
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ---------------- epilogue: warps 2..5 own TMEM lanes 32*(warp%4) ----------------
     const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
+    const int row = quarter * 32 + lane;  // weight row inside the tile
     const int m = m0 + row;
     const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16);
+    const int et = threadIdx.x - 64;      // 0..127
+    float* part = g.partial + (size_t(tile) * g.ks + ks_id) * NA * NT * BM;
+    if (kb1 > kb0) {
+      mbar_wait(tmem_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    if (g.ks == 1) {
+      // direct epilogue from TMEM
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      uint32_t r0[16], r1[16];
-      tmem_ld16(lane_addr + uint32_t(c), r0);
-      if constexpr (NB == 2) tmem_ld16(lane_addr + uint32_t(BN + c), r1);
-      if (m >= g.m_valid) continue;
-      if (g.mode == kDownAcc) {
-        float* yr = g.y + int64_t(m) * g.ldy + n0 + c;
+      for (int c = 0; c < NT; c += 16) {
+        uint32_t r0[16], r1[16];
+        tmem_ld16(lane_addr + uint32_t(c), r0);
+        if constexpr (NA == 2) tmem_ld16(lane_addr + uint32_t(NT + c), r1);
+        if (m >= g.rows) continue;
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          if (n0 + c + e < g.n_valid) {
-            const float v = __uint_as_float(r0[e]);
-            yr[e] = g.accumulate ? yr[e] + v : v;
+          const int t = t0 + c + e;
+          if (t >= g.T) break;
+          if (g.mode == kDown) {
+            float* yp = g.y + int64_t(t) * g.ldy + m;
+            *yp += __uint_as_float(r0[e]);
+          } else {
+            float v = act_fn(g.act, __uint_as_float(r0[e]));
+            if constexpr (NA == 2) v *= __uint_as_float(r1[e]);
+            g.a_out[int64_t(t) * g.lda + m] = __float2bfloat16_rn(v);
           }
         }
-      } else {
-        __nv_bfloat16* ar = g.a_out + int64_t(m) * g.lda + g.a_col0 + n0 + c;
+      }
+    } else {
+      // split-K: partial [NA][NT][128] (coalesced over rows), then the last split fixes up
+#pragma unroll 1
+      for (int c = 0; c < NT; c += 16) {
+        uint32_t r[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          if (n0 + c + e < g.n_valid) {
-            float v = act_fn(g.act, __uint_as_float(r0[e]));
-            if constexpr (NB == 2) v *= __uint_as_float(r1[e]);
-            ar[e] = __float2bfloat16_rn(v);
+        for (int a = 0; a < NA; ++a) {
+          if (kb1 > kb0) {
+            tmem_ld16(lane_addr + uint32_t(a * NT + c), r);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[e] = 0u;
+          }
+#pragma unroll
+          for (int e = 0; e < 16; ++e) part[(size_t(a) * NT + c + e) * BM + row] = __uint_as_float(r[e]);
+        }
+      }
+      __threadfence();
+      epilogue_sync();
+      if (et == 0) {
+        const int ticket = atomicAdd(&g.tickets[tile], 1);
+        *last_flag = ticket == g.ks - 1;
+        if (ticket == g.ks - 1) g.tickets[tile] = 0;  // re-arm for the next launch
+      }
+      epilogue_sync();
+      if (*last_flag) {
+        __threadfence();
+        const float* base = g.partial + size_t(tile) * g.ks * NA * NT * BM;
+        for (int t = 0; t < NT && t0 + t < g.T; ++t) {
+          float v[NA];
+#pragma unroll
+          for (int a = 0; a < NA; ++a) {
+            v[a] = 0.f;
+            for (int q = 0; q < g.ks; ++q)
+              v[a] += __ldcg(base + ((size_t(q) * NA + a) * NT + t) * BM + row);
+          }
+          if (m >= g.rows) continue;
+          if (g.mode == kDown) {
+            g.y[int64_t(t0 + t) * g.ldy + m] += v[0];
+          } else {
+            float o = act_fn(g.act, v[0]);
+            if constexpr (NA == 2) o *= v[NA - 1];
+            g.a_out[int64_t(t0 + t) * g.lda + m] = __float2bfloat16_rn(o);
           }
         }
       }
@@ -236,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// gather x rows (any dtype) into a contiguous bf16 [T_pad, ldx] buffer
+// gather x rows (any dtype) into a contiguous bf16 [T, ldo] buffer
 __global__ void gather_rows_bf16_kernel(const void* x, int xdtype, int64_t ldx_in, const int32_t* ids, int t0,
                                         int T, int M, __nv_bfloat16* out, int64_t ldo) {
   const int t = blockIdx.y;

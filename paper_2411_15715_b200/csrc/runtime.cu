@@ -138,6 +138,8 @@ struct Context {
   DevBuf ws;         // device workspace
   PinnedBuf hpin;    // pinned host staging (ids/gates, x, y_cc, y)
   PinnedBuf xroute;  // x read back for the MoE router (and reused by the CC blocks)
+  DevBuf tc_partial;  // split-K partial tiles of the tensor-core GEMMs
+  DevBuf tc_tickets;  // per-tile split tickets (zero, re-armed by the last split)
   std::vector<float> hscratch;
   std::unique_ptr<ThreadPool> pool;
   int host_threads = 1;
@@ -443,28 +445,60 @@ static int make_tmap(CUtensorMap* map, const void* base, int64_t inner, int64_t 
   return SP_OK;
 }
 
-template <int BN, int NB>
-static int launch_gemm(Context* C, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
-                       tc::GemmArgs g, cudaStream_t s) {
-  auto kern = tc::gemm_kernel<BN, NB>;
-  constexpr int STAGE = tc::BM * tc::BK * 2 + NB * BN * tc::BK * 2;
+template <int NT, int NA>
+static int launch_gemm_t(Context* C, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
+                         tc::GemmArgs g, cudaStream_t s) {
+  auto kern = tc::gemm_kernel<NT, NA>;
+  constexpr int STAGE = NA * tc::BM * tc::BK * 2 + NT * tc::BK * 2;
   static bool attr_set = false;
   if (!attr_set) {
     SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
     attr_set = true;
   }
-  g.stages = std::min(6, (kSmemLimit - 1024 - 256) / STAGE);
+  const int ctas = g.m_tiles * g.t_tiles * g.ks;
+  // one CTA per SM with a deep ring, or two per SM with a shallow one
+  const int budget = ctas <= C->num_sms ? kSmemLimit : kSmemLimit / 2 - 1024;
+  g.stages = std::max(2, std::min(6, (budget - 1024 - 256) / STAGE));
   const size_t smem = size_t(g.stages) * STAGE + 1024 + 256;
-  dim3 grid(unsigned((g.n_valid + BN - 1) / BN), unsigned((g.m_valid + tc::BM - 1) / tc::BM));
-  kern<<<grid, tc::kThreads, smem, s>>>(a, b0, b1, g);
+  if (g.ks > 1) {
+    const size_t need = size_t(g.m_tiles) * g.t_tiles * g.ks * NA * NT * tc::BM * 4;
+    SP_TRY(C->tc_partial.ensure(need));
+    g.partial = static_cast<float*>(C->tc_partial.p);
+    const size_t tk = size_t(g.m_tiles) * g.t_tiles * 4;
+    if (tk > C->tc_tickets.n) {
+      SP_TRY(C->tc_tickets.ensure(tk));
+      SP_CUDA(cudaMemsetAsync(C->tc_tickets.p, 0, C->tc_tickets.n, s));
+    }
+    g.tickets = static_cast<int*>(C->tc_tickets.p);
+  }
+  kern<<<ctas, tc::kThreads, smem, s>>>(a0, a1, b, g);
   SP_CUDA(cudaGetLastError());
   ++C->launches;
   return SP_OK;
 }
 
+template <int NA>
+static int launch_gemm(Context* C, int nt, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
+                       const tc::GemmArgs& g, cudaStream_t s) {
+  switch (nt) {
+    case 16: return launch_gemm_t<16, NA>(C, a0, a1, b, g, s);
+    case 32: return launch_gemm_t<32, NA>(C, a0, a1, b, g, s);
+    case 64: return launch_gemm_t<64, NA>(C, a0, a1, b, g, s);
+    case 128: return launch_gemm_t<128, NA>(C, a0, a1, b, g, s);
+    default: return launch_gemm_t<256, NA>(C, a0, a1, b, g, s);
+  }
+}
+
+// Split K so the launch puts ~`target` CTAs to work (bounded by the k-blocks).
+static int split_k(int tiles, int k, int target) {
+  const int nkb = (k + tc::BK - 1) / tc::BK;
+  return std::max(1, std::min(nkb, target / std::max(1, tiles)));
+}
+
 // up GEMM (fused SwiGLU / act) into a_tc, then down GEMM accumulated into the call's tc slice
 static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype, int64_t ldx,
-                        CallWs& w, const int32_t* dev_ids, int64_t T_e, int t0, int T, cudaStream_t s) {
+                        CallWs& w, const int32_t* dev_ids, int64_t T_e, int t0, int T, cudaStream_t s,
+                        bool resident) {
   const int64_t M = L->d.model_dim, N = L->d.out_dim, R = b.rows;
   if (w.tc_slice < 0) {
     w.tc_slice = w.S++;
@@ -477,34 +511,42 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
     SP_CUDA(cudaGetLastError());
     ++C->launches;
   }
+  const int nt = T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256;
+  const int t_tiles = int((T + nt - 1) / nt);
+  // HBM-resident blocks spread over every SM; streamed chunks hide under their copy
+  const int target = resident ? C->num_sms : 32;
   CUtensorMap tx, tw1, tw3, ta, tw2;
-  SP_TRY(make_tmap(&tx, w.x_tc, M, T, L->ldm * 2, tc::BK, tc::BM));
-  SP_TRY(make_tmap(&tw1, b.base, M, R, L->ldm * 2, tc::BK, 64));
-  SP_TRY(make_tmap(&tw3, L->d.gated ? b.base + b.w3_off : b.base, M, R, L->ldm * 2, tc::BK, 64));
+  SP_TRY(make_tmap(&tw1, b.base, M, R, L->ldm * 2, tc::BK, tc::BM));
+  SP_TRY(make_tmap(&tw3, L->d.gated ? b.base + b.w3_off : b.base, M, R, L->ldm * 2, tc::BK, tc::BM));
+  SP_TRY(make_tmap(&tx, w.x_tc, M, T, L->ldm * 2, tc::BK, nt));
   tc::GemmArgs up{};
-  up.m_valid = T;
-  up.n_valid = int(R);
-  up.k = int(M);
   up.mode = L->d.gated ? tc::kUpGated : tc::kUpPlain;
   up.act = L->d.act;
+  up.rows = int(R);
+  up.T = T;
+  up.k = int(M);
+  up.m_tiles = int((R + tc::BM - 1) / tc::BM);
+  up.t_tiles = t_tiles;
+  up.ks = split_k(up.m_tiles * t_tiles, int(M), target);
   up.a_out = w.a_tc;
   up.lda = w.ld_a;
-  up.a_col0 = 0;
   if (L->d.gated)
-    SP_TRY((launch_gemm<64, 2>(C, tx, tw1, tw3, up, s)));
+    SP_TRY(launch_gemm<2>(C, nt, tw1, tw3, tx, up, s));
   else
-    SP_TRY((launch_gemm<64, 1>(C, tx, tw1, tw1, up, s)));
-  SP_TRY(make_tmap(&ta, w.a_tc, R, T, w.ld_a * 2, tc::BK, tc::BM));
+    SP_TRY(launch_gemm<1>(C, nt, tw1, tw1, tx, up, s));
   SP_TRY(make_tmap(&tw2, b.base + b.w2_off, N, R, L->ldn * 2, 64, tc::BK));
+  SP_TRY(make_tmap(&ta, w.a_tc, R, T, w.ld_a * 2, tc::BK, nt));
   tc::GemmArgs dn{};
-  dn.m_valid = T;
-  dn.n_valid = int(N);
+  dn.mode = tc::kDown;
+  dn.rows = int(N);
+  dn.T = T;
   dn.k = int(R);
-  dn.mode = tc::kDownAcc;
+  dn.m_tiles = int((N + tc::BM - 1) / tc::BM);
+  dn.t_tiles = t_tiles;
+  dn.ks = split_k(dn.m_tiles * t_tiles, int(R), target);
   dn.y = w.part + size_t(w.tc_slice) * T_e * N + size_t(t0) * N;
   dn.ldy = N;
-  dn.accumulate = 1;
-  return launch_gemm<64, 1>(C, ta, tw2, tw2, dn, s);
+  return launch_gemm<1>(C, nt, tw2, tw2, ta, dn, s);
 }
 
 static FfnArgs ffn_args(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,
@@ -548,7 +590,7 @@ static int run_block(Context* C, const sp_layer* L, const BlockView& b, const vo
                      int64_t ldx, CallWs& w, const int32_t* host_ids, int64_t T_e, int t0, int T,
                      cudaStream_t s, int min_rows = g_min_rows_per_cta) {
   if (L->d.wdtype == SP_BF16 && T >= g_tc_min_tokens && w.x_tc && w.a_tc)
-    return run_block_tc(C, L, b, x, xdtype, ldx, w, w.ids, T_e, t0, T, s);
+    return run_block_tc(C, L, b, x, xdtype, ldx, w, w.ids, T_e, t0, T, s, min_rows == g_min_rows_per_cta);
   const int grid = block_grid(C, b.rows, min_rows);
   const int tt_max = max_token_tile(L->d.model_dim);
   if (tt_max == 0) return fail(SP_ERR_VALUE, "model_dim %lld exceeds the x tile", (long long)L->d.model_dim);
