@@ -57,7 +57,7 @@ struct GemmArgs {
   // down epilogue: y[t * ldy + n] += acc  (fp32, the call's tensor-core slice)
   float* y;
   int64_t ldy;
-  // split-K partials [tile][ks][NA][NT][128] fp32 and tickets [tile]
+  // split-K partials [tile][ks][NA][128][NT] fp32 and tickets [tile]
   float* partial;
   int* tickets;
 };
@@ -245,7 +245,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else {
-      // split-K: partial [NA][NT][128] (coalesced over rows), then the last split fixes up
+      // split-K: partial [NA][128 rows][NT] (a row's tokens contiguous -> float4), then the
+      // last split of the tile sums the KS partials in split order and runs the epilogue
+      float* prow = part + size_t(row) * NT;
 #pragma unroll 1
       for (int c = 0; c < NT; c += 16) {
         uint32_t r[16];
@@ -257,8 +259,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 16; ++e) r[e] = 0u;
           }
+          float4* dst = reinterpret_cast<float4*>(prow + size_t(a) * BM * NT + c);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) part[(size_t(a) * NT + c + e) * BM + row] = __uint_as_float(r[e]);
+          for (int e = 0; e < 4; ++e)
+            dst[e] = make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
+                                 __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3]));
         }
       }
       __threadfence();
@@ -271,22 +276,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       epilogue_sync();
       if (*last_flag) {
         __threadfence();
-        const float* base = g.partial + size_t(tile) * g.ks * NA * NT * BM;
-        for (int t = 0; t < NT && t0 + t < g.T; ++t) {
-          float v[NA];
+        const float* base = g.partial + size_t(tile) * g.ks * NA * NT * BM + size_t(row) * NT;
+#pragma unroll 1
+        for (int c = 0; c < NT && t0 + c < g.T; c += 16) {
+          float4 acc[NA][4];
 #pragma unroll
-          for (int a = 0; a < NA; ++a) {
-            v[a] = 0.f;
-            for (int q = 0; q < g.ks; ++q)
-              v[a] += __ldcg(base + ((size_t(q) * NA + a) * NT + t) * BM + row);
+          for (int a = 0; a < NA; ++a)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[a][e] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int q = 0; q < g.ks; ++q) {
+            float4 v[NA][4];
+#pragma unroll
+            for (int a = 0; a < NA; ++a)
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                v[a][e] = __ldcg(reinterpret_cast<const float4*>(base + (size_t(q) * NA + a) * BM * NT + c) + e);
+#pragma unroll
+            for (int a = 0; a < NA; ++a)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                acc[a][e].x += v[a][e].x;
+                acc[a][e].y += v[a][e].y;
+                acc[a][e].z += v[a][e].z;
+                acc[a][e].w += v[a][e].w;
+              }
           }
           if (m >= g.rows) continue;
-          if (g.mode == kDown) {
-            g.y[int64_t(t0 + t) * g.ldy + m] += v[0];
-          } else {
-            float o = act_fn(g.act, v[0]);
-            if constexpr (NA == 2) o *= v[NA - 1];
-            g.a_out[int64_t(t0 + t) * g.lda + m] = __float2bfloat16_rn(o);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int t = t0 + c + e;
+            if (t >= g.T) break;
+            const float v0 = reinterpret_cast<const float*>(&acc[0][0])[e];
+            if (g.mode == kDown) {
+              g.y[int64_t(t) * g.ldy + m] += v0;
+            } else {
+              float o = act_fn(g.act, v0);
+              if constexpr (NA == 2) o *= reinterpret_cast<const float*>(&acc[NA - 1][0])[e];
+              g.a_out[int64_t(t) * g.lda + m] = __float2bfloat16_rn(o);
+            }
           }
         }
       }
