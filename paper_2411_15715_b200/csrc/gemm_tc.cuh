@@ -54,9 +54,13 @@ struct GemmArgs {
   // up epilogue: a[t * lda + h]  (bf16)
   __nv_bfloat16* a_out;
   int64_t lda;
-  // down epilogue: y[t * ldy + n] += acc  (fp32, the call's tensor-core slice)
+  // down epilogue: y[t * ldy + n] += acc  (fp32, the call's tensor-core slice), or with
+  // split_slices: split q STORES its partial into y + q * y_split_stride (one output
+  // slice per split; finalize_kernel sums the slices in order -- no fix-up pass)
   float* y;
   int64_t ldy;
+  int split_slices;
+  int64_t y_split_stride;
   // split-K partials [tile][ks][NA][128][NT] fp32 and tickets [tile]
   float* partial;
   int* tickets;
@@ -117,8 +121,11 @@ __device__ __forceinline__ void epilogue_sync() {
   asm volatile("bar.sync 2, 128;" ::: "memory");
 }
 
-// NT: tokens per tile (UMMA N, multiple of 16, <= 256); NA: A operands (2 = W1t + W3t)
-template <int NT, int NA>
+// NT: tokens per tile (UMMA N, multiple of 16, <= 256).  NA A-tiles share one B tile,
+// each with its own TMEM accumulator: up -> W1t and W3t rows of the same 128
+// hidden units (NA = 2 gated); down -> NA consecutive 128-column sub-tiles of W2
+// (one fetch of `a` per k-block feeds NA MMAs; W2 rows are read NA*256 bytes at a time).
+template <int NT, int NA, bool DOWN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                 const __grid_constant__ CUtensorMap tmB, const GemmArgs g) {
@@ -141,10 +148,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ks_id = blockIdx.x % g.ks;
   const int tile = blockIdx.x / g.ks;  // = tt * m_tiles + mt
   const int mt = tile % g.m_tiles, tt = tile / g.m_tiles;
-  const int m0 = mt * BM, t0 = tt * NT;
+  const int m0 = mt * BM * (DOWN ? NA : 1), t0 = tt * NT;
   const int nkb = (g.k + BK - 1) / BK;
   const int kb0 = nkb * ks_id / g.ks, kb1 = nkb * (ks_id + 1) / g.ks;
-  const bool a_mn = g.mode == kDown;
+  constexpr bool a_mn = DOWN;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -175,13 +182,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
         unsigned char* st = smem + size_t(s) * STAGE;
         mbar_expect_tx(&full[s], STAGE);
-        if (!a_mn) {
+        if constexpr (!DOWN) {
           tma_load_2d(st, &tmA0, &full[s], kb * BK, m0);
           if constexpr (NA == 2) tma_load_2d(st + A_BYTES, &tmA1, &full[s], kb * BK, m0);
         } else {
-          // MN-major A (W2 [k rows][n]): two 64-column boxes of BK rows
-          tma_load_2d(st, &tmA0, &full[s], m0, kb * BK);
-          tma_load_2d(st + BK * 128, &tmA0, &full[s], m0 + 64, kb * BK);
+          // MN-major A (W2 [k rows][n]): per sub-tile two 64-column boxes of BK rows
+#pragma unroll
+          for (int a = 0; a < NA; ++a) {
+            tma_load_2d(st + a * A_BYTES, &tmA0, &full[s], m0 + a * BM, kb * BK);
+            tma_load_2d(st + a * A_BYTES + BK * 128, &tmA0, &full[s], m0 + a * BM + 64, kb * BK);
+          }
         }
         tma_load_2d(st + NA * A_BYTES, &tmB, &full[s], kb * BK, t0);
       }
@@ -200,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t b = umma_desc(st + NA * A_BYTES + kk * 32, 16, 1024);
 #pragma unroll
           for (int a = 0; a < NA; ++a) {
-            const uint64_t ad = a_mn ? umma_desc(st + kk * UK * 128, BK * 128, 1024)
+            const uint64_t ad = a_mn ? umma_desc(st + a * A_BYTES + kk * UK * 128, BK * 128, 1024)
                                      : umma_desc(st + a * A_BYTES + kk * 32, 16, 1024);
             umma_bf16(tmem + uint32_t(a * NT), ad, b, idesc, (i > 0 || kk > 0) ? 1u : 0u);
           }
@@ -222,24 +232,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(tmem_full, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
-    if (g.ks == 1) {
-      // direct epilogue from TMEM
+    if (DOWN && g.split_slices) {
+      float* ys = g.y + int64_t(ks_id) * g.y_split_stride;
 #pragma unroll 1
       for (int c = 0; c < NT; c += 16) {
-        uint32_t r0[16], r1[16];
-        tmem_ld16(lane_addr + uint32_t(c), r0);
-        if constexpr (NA == 2) tmem_ld16(lane_addr + uint32_t(NT + c), r1);
-        if (m >= g.rows) continue;
+        uint32_t r[NA][16];
+#pragma unroll
+        for (int a = 0; a < NA; ++a) {
+          if (kb1 > kb0) {
+            tmem_ld16(lane_addr + uint32_t(a * NT + c), r[a]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[a][e] = 0u;
+          }
+        }
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int t = t0 + c + e;
           if (t >= g.T) break;
-          if (g.mode == kDown) {
-            float* yp = g.y + int64_t(t) * g.ldy + m;
-            *yp += __uint_as_float(r0[e]);
+#pragma unroll
+          for (int a = 0; a < NA; ++a) {
+            const int mm = m + a * BM;
+            if (mm < g.rows) ys[int64_t(t) * g.ldy + mm] = __uint_as_float(r[a][e]);
+          }
+        }
+      }
+    } else if (g.ks == 1) {
+      // direct epilogue from TMEM
+#pragma unroll 1
+      for (int c = 0; c < NT; c += 16) {
+        uint32_t r[NA][16];
+#pragma unroll
+        for (int a = 0; a < NA; ++a) tmem_ld16(lane_addr + uint32_t(a * NT + c), r[a]);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int t = t0 + c + e;
+          if (t >= g.T) break;
+          if constexpr (DOWN) {
+#pragma unroll
+            for (int a = 0; a < NA; ++a) {
+              const int mm = m + a * BM;
+              if (mm < g.rows) g.y[int64_t(t) * g.ldy + mm] += __uint_as_float(r[a][e]);
+            }
           } else {
-            float v = act_fn(g.act, __uint_as_float(r0[e]));
-            if constexpr (NA == 2) v *= __uint_as_float(r1[e]);
+            if (m >= g.rows) continue;
+            float v = act_fn(g.act, __uint_as_float(r[0][e]));
+            if constexpr (NA == 2) v *= __uint_as_float(r[1][e]);
             g.a_out[int64_t(t) * g.lda + m] = __float2bfloat16_rn(v);
           }
         }
@@ -301,16 +339,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc[a][e].w += v[a][e].w;
               }
           }
-          if (m >= g.rows) continue;
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             const int t = t0 + c + e;
             if (t >= g.T) break;
-            const float v0 = reinterpret_cast<const float*>(&acc[0][0])[e];
-            if (g.mode == kDown) {
-              g.y[int64_t(t) * g.ldy + m] += v0;
+            if constexpr (DOWN) {
+#pragma unroll
+              for (int a = 0; a < NA; ++a) {
+                const int mm = m + a * BM;
+                if (mm < g.rows) g.y[int64_t(t) * g.ldy + mm] += reinterpret_cast<const float*>(&acc[a][0])[e];
+              }
             } else {
-              float o = act_fn(g.act, v0);
+              if (m >= g.rows) continue;
+              float o = act_fn(g.act, reinterpret_cast<const float*>(&acc[0][0])[e]);
               if constexpr (NA == 2) o *= reinterpret_cast<const float*>(&acc[NA - 1][0])[e];
               g.a_out[int64_t(t) * g.lda + m] = __float2bfloat16_rn(o);
             }

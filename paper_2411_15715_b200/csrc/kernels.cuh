@@ -484,74 +484,102 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
 }
 
 // ---- finalize: slice reduction + CC partial + MoE gates + cast, one launch -------------
-//   y[t, n] = sum_c sum_{i: ids_c[i] = t} gate_c[i] * (sum_s part_c[s, i, n] + y_cc_c[i, n])
-// Block = 32 output columns x 8 slice groups.  Every column is owned by one
-// block and every sum runs in a fixed order, so results are deterministic.
+//   y[t, n] = sum over entries (c, i, gate) of token t (host-built CSR, in call order)
+//             of gate * (sum_s part_c[s, i, n] + y_cc_c[i, n])
+// Block = (128 output columns as 32 float4 lanes) x 8 slice groups, one output
+// token per blockIdx.y.  Every sum runs in a fixed order -> deterministic.
 constexpr int kMaxCalls = 32;
 struct FinalCall {
   const float* part;     // [S][T_e][N] partial slices
   int S;
   const float* y_cc;     // [T_e, N] or null; rows >= n_cc are absent
   int n_cc;
-  const int32_t* ids;    // device [T_e] or null (identity)
-  const float* gates;    // device [T_e] or null (1.0)
   int T_e;
 };
 struct FinalArgs {
   FinalCall c[kMaxCalls];
-  int n_calls;
+  const int* entry_start;  // device [T + 1]
+  const int* entry_call;   // device [entries]
+  const int* entry_row;    // device [entries]
+  const float* entry_gate; // device [entries]
   int T;
   int N;
-  float* acc;   // [T, N] fp32 scratch (also the output when odtype == f32)
   void* out;    // [T, N] in odtype
   int odtype;
 };
 
 __global__ void __launch_bounds__(256) finalize_kernel(FinalArgs p) {
-  __shared__ float red[8][33];
-  const int col = threadIdx.x & 31, grp = threadIdx.x >> 5;
-  const int n = blockIdx.x * 32 + col;
-  const bool live = n < p.N;
-  if (grp == 0 && live)
-    for (int t = 0; t < p.T; ++t) p.acc[int64_t(t) * p.N + n] = 0.f;
-  for (int c = 0; c < p.n_calls; ++c) {
-    const FinalCall& fc = p.c[c];
-    for (int i = 0; i < fc.T_e; ++i) {
-      float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
-      if (live) {
-        const float* base = fc.part + int64_t(i) * p.N + n;
-        const int64_t stride = int64_t(fc.T_e) * p.N;
-        int s = grp;
-        for (; s + 24 < fc.S; s += 32) {
-          v0 += base[int64_t(s) * stride];
-          v1 += base[int64_t(s + 8) * stride];
-          v2 += base[int64_t(s + 16) * stride];
-          v3 += base[int64_t(s + 24) * stride];
-        }
-        for (; s < fc.S; s += 8) v0 += base[int64_t(s) * stride];
+  __shared__ float4 red[8][32];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int n = (blockIdx.x * 32 + lane) * 4;
+  const int t = blockIdx.y;
+  const bool live = n < p.N;  // N % 4 == 0 on this path
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int e = p.entry_start[t]; e < p.entry_start[t + 1]; ++e) {
+    const FinalCall& fc = p.c[p.entry_call[e]];
+    const int i = p.entry_row[e];
+    float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+    if (live) {
+      const int64_t stride = int64_t(fc.T_e) * p.N;
+      const float* base = fc.part + int64_t(i) * p.N + n;
+      int s = grp;
+      for (; s + 8 < fc.S; s += 16) {
+        const float4 a = __ldcg(reinterpret_cast<const float4*>(base + int64_t(s) * stride));
+        const float4 b = __ldcg(reinterpret_cast<const float4*>(base + int64_t(s + 8) * stride));
+        v0.x += a.x; v0.y += a.y; v0.z += a.z; v0.w += a.w;
+        v1.x += b.x; v1.y += b.y; v1.z += b.z; v1.w += b.w;
       }
-      red[grp][col] = (v0 + v1) + (v2 + v3);
-      __syncthreads();
-      if (grp == 0 && live) {
-        float tot = 0.f;
-#pragma unroll
-        for (int g = 0; g < 8; ++g) tot += red[g][col];
-        if (fc.y_cc && i < fc.n_cc) tot += fc.y_cc[int64_t(i) * p.N + n];
-        const int t = fc.ids ? fc.ids[i] : i;
-        const float gate = fc.gates ? fc.gates[i] : 1.0f;
-        p.acc[int64_t(t) * p.N + n] += gate * tot;
+      for (; s < fc.S; s += 8) {
+        const float4 a = __ldcg(reinterpret_cast<const float4*>(base + int64_t(s) * stride));
+        v0.x += a.x; v0.y += a.y; v0.z += a.z; v0.w += a.w;
       }
-      __syncthreads();
     }
+    red[grp][lane] = make_float4(v0.x + v1.x, v0.y + v1.y, v0.z + v1.z, v0.w + v1.w);
+    __syncthreads();
+    if (grp == 0 && live) {
+      float4 tot = red[0][lane];
+#pragma unroll
+      for (int g = 1; g < 8; ++g) {
+        const float4 r = red[g][lane];
+        tot.x += r.x; tot.y += r.y; tot.z += r.z; tot.w += r.w;
+      }
+      if (fc.y_cc && i < fc.n_cc) {
+        const float4 c = *reinterpret_cast<const float4*>(fc.y_cc + int64_t(i) * p.N + n);
+        tot.x += c.x; tot.y += c.y; tot.z += c.z; tot.w += c.w;
+      }
+      const float gate = p.entry_gate[e];
+      acc.x += gate * tot.x; acc.y += gate * tot.y; acc.z += gate * tot.z; acc.w += gate * tot.w;
+    }
+    __syncthreads();
   }
   if (grp == 0 && live) {
     if (p.odtype == 1) {
-      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out);
-      for (int t = 0; t < p.T; ++t) o[int64_t(t) * p.N + n] = __float2bfloat16_rn(p.acc[int64_t(t) * p.N + n]);
-    } else if (p.out != p.acc) {
-      float* o = static_cast<float*>(p.out);
-      for (int t = 0; t < p.T; ++t) o[int64_t(t) * p.N + n] = p.acc[int64_t(t) * p.N + n];
+      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.out) + int64_t(t) * p.N + n);
+      o[0] = __floats2bfloat162_rn(acc.x, acc.y);
+      o[1] = __floats2bfloat162_rn(acc.z, acc.w);
+    } else {
+      *reinterpret_cast<float4*>(static_cast<float*>(p.out) + int64_t(t) * p.N + n) = acc;
     }
+  }
+}
+
+// Same contract for N % 4 != 0 (small test shapes): one thread per output element.
+__global__ void __launch_bounds__(256) finalize_scalar_kernel(FinalArgs p) {
+  const int t = blockIdx.y;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < p.N; n += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int e = p.entry_start[t]; e < p.entry_start[t + 1]; ++e) {
+      const FinalCall& fc = p.c[p.entry_call[e]];
+      const int i = p.entry_row[e];
+      float tot = 0.f;
+      for (int s = 0; s < fc.S; ++s) tot += fc.part[(int64_t(s) * fc.T_e + i) * p.N + n];
+      if (fc.y_cc && i < fc.n_cc) tot += fc.y_cc[int64_t(i) * p.N + n];
+      acc += p.entry_gate[e] * tot;
+    }
+    if (p.odtype == 1)
+      static_cast<__nv_bfloat16*>(p.out)[int64_t(t) * p.N + n] = __float2bfloat16_rn(acc);
+    else
+      static_cast<float*>(p.out)[int64_t(t) * p.N + n] = acc;
   }
 }
 

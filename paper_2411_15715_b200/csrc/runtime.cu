@@ -404,6 +404,7 @@ struct CallWs {
   float* part;     // [S][T_e][N] partial slices of every block of the call
   int S;           // slices in use
   int tc_slice = -1;            // slice the tensor-core blocks accumulate into
+  int split_capacity = 0;       // spare slices for split-K partials of resident tc blocks
   __nv_bfloat16* x_tc = nullptr;  // [T_e, ldm] gathered bf16 x (tensor-core path)
   __nv_bfloat16* a_tc = nullptr;  // [T_e, ld_a] bf16 hidden activations of one block
   int64_t ld_a = 0;
@@ -414,6 +415,7 @@ struct CallWs {
 
 // ---- tensor-core (tcgen05) block path for many tokens -------------------------
 static const int g_tc_min_tokens = env_int("SP_TC_MIN_T", 16);
+constexpr int kTcMaxSplits = 24;  // split-K output slices a resident tc block may use
 
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -445,10 +447,10 @@ static int make_tmap(CUtensorMap* map, const void* base, int64_t inner, int64_t 
   return SP_OK;
 }
 
-template <int NT, int NA>
+template <int NT, int NA, bool DOWN>
 static int launch_gemm_t(Context* C, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
                          tc::GemmArgs g, cudaStream_t s) {
-  auto kern = tc::gemm_kernel<NT, NA>;
+  auto kern = tc::gemm_kernel<NT, NA, DOWN>;
   constexpr int STAGE = NA * tc::BM * tc::BK * 2 + NT * tc::BK * 2;
   static bool attr_set = false;
   if (!attr_set) {
@@ -477,15 +479,17 @@ static int launch_gemm_t(Context* C, const CUtensorMap& a0, const CUtensorMap& a
   return SP_OK;
 }
 
-template <int NA>
+template <int NA, bool DOWN>
 static int launch_gemm(Context* C, int nt, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
                        const tc::GemmArgs& g, cudaStream_t s) {
   switch (nt) {
-    case 16: return launch_gemm_t<16, NA>(C, a0, a1, b, g, s);
-    case 32: return launch_gemm_t<32, NA>(C, a0, a1, b, g, s);
-    case 64: return launch_gemm_t<64, NA>(C, a0, a1, b, g, s);
-    case 128: return launch_gemm_t<128, NA>(C, a0, a1, b, g, s);
-    default: return launch_gemm_t<256, NA>(C, a0, a1, b, g, s);
+    case 16: return launch_gemm_t<16, NA, DOWN>(C, a0, a1, b, g, s);
+    case 32: return launch_gemm_t<32, NA, DOWN>(C, a0, a1, b, g, s);
+    case 64: return launch_gemm_t<64, NA, DOWN>(C, a0, a1, b, g, s);
+    case 128: return launch_gemm_t<128, NA, DOWN>(C, a0, a1, b, g, s);
+    default:
+      if constexpr (NA <= 2) return launch_gemm_t<256, NA, DOWN>(C, a0, a1, b, g, s);
+      return fail(SP_ERR_VALUE, "token tile 256 with %d sub-tiles exceeds TMEM", NA);
   }
 }
 
@@ -531,9 +535,9 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
   up.a_out = w.a_tc;
   up.lda = w.ld_a;
   if (L->d.gated)
-    SP_TRY(launch_gemm<2>(C, nt, tw1, tw3, tx, up, s));
+    SP_TRY((launch_gemm<2, false>(C, nt, tw1, tw3, tx, up, s)));
   else
-    SP_TRY(launch_gemm<1>(C, nt, tw1, tw1, tx, up, s));
+    SP_TRY((launch_gemm<1, false>(C, nt, tw1, tw1, tx, up, s)));
   SP_TRY(make_tmap(&tw2, b.base + b.w2_off, N, R, L->ldn * 2, 64, tc::BK));
   SP_TRY(make_tmap(&ta, w.a_tc, R, T, w.ld_a * 2, tc::BK, nt));
   tc::GemmArgs dn{};
@@ -541,12 +545,25 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
   dn.rows = int(N);
   dn.T = T;
   dn.k = int(R);
-  dn.m_tiles = int((N + tc::BM - 1) / tc::BM);
+  // 2 column sub-tiles per CTA share each fetched `a` tile
+  constexpr int sub = 2;
+  dn.m_tiles = int((N + tc::BM * sub - 1) / (tc::BM * sub));
   dn.t_tiles = t_tiles;
-  dn.ks = split_k(dn.m_tiles * t_tiles, int(R), target);
-  dn.y = w.part + size_t(w.tc_slice) * T_e * N + size_t(t0) * N;
   dn.ldy = N;
-  return launch_gemm<1>(C, nt, tw2, tw2, ta, dn, s);
+  if (resident) {
+    // HBM-resident block: split K over ~every SM, one output slice per split
+    dn.ks = std::min(split_k(dn.m_tiles * t_tiles, int(R), target), w.split_capacity);
+    dn.split_slices = 1;
+    dn.y_split_stride = int64_t(T_e) * N;
+    if (t0 > 0 || T < T_e)  // rows outside [t0, t0 + T) of the new slices must read as zero
+      SP_CUDA(cudaMemsetAsync(w.part + size_t(w.S) * T_e * N, 0, size_t(dn.ks) * T_e * N * 4, s));
+    dn.y = w.part + size_t(w.S) * T_e * N + size_t(t0) * N;
+    w.S += dn.ks;
+  } else {
+    dn.ks = 1;  // streamed chunk: hidden under its copy, accumulate into the tc slice
+    dn.y = w.part + size_t(w.tc_slice) * T_e * N + size_t(t0) * N;
+  }
+  return launch_gemm<sub, true>(C, nt, tw2, tw2, ta, dn, s);
 }
 
 static FfnArgs ffn_args(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,
@@ -781,11 +798,14 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   std::vector<size_t> o_part(n_calls), o_ycc(n_calls), o_ids(n_calls), o_g(n_calls), o_xtc(n_calls),
       o_atc(n_calls);
   std::vector<int64_t> ws_ld_a(n_calls);
+  std::vector<int> ws_split(n_calls, 0);
   int64_t total_rows = 0;
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int64_t Te = calls[c].tokens;
-    int64_t slices = block_grid(C, L->h_gg) + 1;  // + the tensor-core accumulation slice
+    const bool tc_call = L->d.wdtype == SP_BF16 && Te >= g_tc_min_tokens;
+    ws_split[c] = tc_call ? kTcMaxSplits : 0;
+    int64_t slices = block_grid(C, L->h_gg) + 1 + ws_split[c];  // + tc accumulation slice + tc splits
     for (int ci = 0; ci < int(L->chunks.size()); ++ci)
       if (ci >= L->n_cc_chunks || calls[c].n_g > 0) slices += block_grid(C, L->chunks[ci].rc, g_chunk_min_rows);
     o_part[c] = dalloc(size_t(slices) * Te * N * 4);
@@ -800,7 +820,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     o_g[c] = dalloc(size_t(Te) * 4);
     total_rows += Te;
   }
-  const size_t o_acc = dalloc(size_t(T) * N * 4);
+  const size_t o_csr = dalloc(size_t(T + 1 + 3 * total_rows) * 4);
   const size_t o_xdev = dalloc(host_io ? size_t(T) * M * xel : 0);
   const size_t o_ydev = dalloc(host_io ? size_t(T) * N * yel : 0);
   SP_TRY(C->ws.ensure(dev_off));
@@ -809,6 +829,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     ws[c].part = reinterpret_cast<float*>(dws + o_part[c]);
     ws[c].S = 0;
     ws[c].ld_a = ws_ld_a[c];
+    ws[c].split_capacity = ws_split[c];
     if (o_xtc[c] != SIZE_MAX) {
       ws[c].x_tc = reinterpret_cast<__nv_bfloat16*>(dws + o_xtc[c]);
       ws[c].a_tc = reinterpret_cast<__nv_bfloat16*>(dws + o_atc[c]);
@@ -826,6 +847,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     return o;
   };
   const size_t p_meta = palloc(size_t(total_rows) * 8);
+  const size_t p_csr = palloc(size_t(T + 1 + 3 * total_rows) * 4);
   const size_t p_x = palloc(size_t(T) * M * xel);
   std::vector<size_t> p_ycc(n_calls);
   for (int c = 0; c < n_calls; ++c) p_ycc[c] = palloc(size_t(calls[c].tokens) * N * 4);
@@ -855,6 +877,30 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       }
       mo += Te * 8;
     }
+  }
+
+  // ---- output-row CSR for finalize: entries (call, row, gate) of every token, in call order ----
+  {
+    int32_t* cs = reinterpret_cast<int32_t*>(hp + p_csr);
+    int32_t* ccall = cs + (T + 1);
+    int32_t* crow = ccall + total_rows;
+    float* cgate = reinterpret_cast<float*>(crow + total_rows);
+    std::vector<int32_t> count(size_t(T) + 1, 0);
+    for (int c = 0; c < n_calls; ++c)
+      for (int64_t i = 0; i < calls[c].tokens; ++i) ++count[size_t(calls[c].token_ids ? calls[c].token_ids[i] : i)];
+    cs[0] = 0;
+    for (int64_t t = 0; t < T; ++t) cs[t + 1] = cs[t] + count[size_t(t)];
+    std::vector<int32_t> fill(cs, cs + T);
+    for (int c = 0; c < n_calls; ++c)
+      for (int64_t i = 0; i < calls[c].tokens; ++i) {
+        const int64_t t = calls[c].token_ids ? calls[c].token_ids[i] : i;
+        const int32_t slot = fill[size_t(t)]++;
+        ccall[slot] = c;
+        crow[slot] = int32_t(i);
+        cgate[slot] = calls[c].gates ? calls[c].gates[i] : 1.0f;
+      }
+    SP_CUDA(cudaMemcpyAsync(dws + o_csr, cs, size_t(T + 1 + 3 * total_rows) * 4, cudaMemcpyHostToDevice,
+                            C->s_comp));
   }
 
   // ---- x: device copy for the GPU, host copy for the CC threads ----
@@ -1012,22 +1058,32 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
 
   // ---- finalize: reduce slices + CC partials + gates + cast ----
   FinalArgs fa{};
-  fa.n_calls = n_calls;
   fa.T = int(T);
   fa.N = int(N);
-  fa.acc = reinterpret_cast<float*>(dws + o_acc);
   fa.out = host_io ? static_cast<void*>(dws + o_ydev) : y;
   fa.odtype = ydtype;
+  {
+    const int32_t* cs = reinterpret_cast<const int32_t*>(dws + o_csr);
+    fa.entry_start = cs;
+    fa.entry_call = cs + (T + 1);
+    fa.entry_row = fa.entry_call + total_rows;
+    fa.entry_gate = reinterpret_cast<const float*>(fa.entry_row + total_rows);
+  }
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int64_t Tcc = calls[c].tokens - calls[c].n_g;
     fa.c[c] = FinalCall{ws[c].part, ws[c].S, (L->d.b1 > 0 && Tcc > 0) ? ws[c].ycc : nullptr, int(Tcc),
-                        ws[c].ids, ws[c].gates, int(calls[c].tokens)};
+                        int(calls[c].tokens)};
   }
-  if (ydtype == SP_F32 && !host_io) fa.acc = static_cast<float*>(y);
   {
     GpuSpan span(C, C->s_comp, 2, SP_TRACE_MERGE, 0.0);
-    finalize_kernel<<<unsigned((N + 31) / 32), 256, 0, C->s_comp>>>(fa);
+    if (N % 4 == 0 && reinterpret_cast<uintptr_t>(fa.out) % 16 == 0) {
+      dim3 grid(unsigned((N + 127) / 128), unsigned(T));
+      finalize_kernel<<<grid, 256, 0, C->s_comp>>>(fa);
+    } else {
+      dim3 grid(unsigned(std::min<int64_t>((N + 255) / 256, 64)), unsigned(T));
+      finalize_scalar_kernel<<<grid, 256, 0, C->s_comp>>>(fa);
+    }
     SP_CUDA(cudaGetLastError());
     span.end();
     ++C->launches;
