@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--moe", default="8x22b", choices=["phimoe", "8x22b"], help="cfg5 model")
     ap.add_argument("--layers", type=int, default=32, help="cfg3: layers per forward")
     ap.add_argument("--distinct-layers", type=int, default=8, help="cfg3: distinct weight sets cycled over the layers")
     ap.add_argument("--prompt", type=int, default=512, help="cfg3: prompt tokens")
@@ -70,6 +71,11 @@ def parse():
     args = ap.parse_args()
     if args.config == "cfg1":
         args.model_dim, args.hidden_dim, args.dtype = 1024, 3584, "f32"
+    elif args.config == "cfg4":  # LLaMA-2-70B dense FFN, column-sharded over the ranks
+        args.model_dim, args.hidden_dim, args.dtype, args.experts, args.top_k = 8192, 28672, "bf16", 1, 1
+    elif args.config == "cfg5":  # PhiMoE 16x(4096/6400) or Mixtral-8x22B 8x(6144/16384), top-2
+        args.dtype = "bf16"
+        args.model_dim, args.hidden_dim, args.experts = (4096, 6400, 16) if args.moe == "phimoe" else (6144, 16384, 8)
     else:
         args.model_dim, args.hidden_dim, args.dtype = 4096, 14336, "bf16"
     if args.config == "cfg3" and args.steps == 100:
@@ -78,6 +84,11 @@ def parse():
 
 
 def metric_name(args):
+    if args.config == "cfg4":
+        return "decode tokens/s, LLaMA-2-70B dense FFN layer (8192/28672) bf16, column-sharded, sliced CC/CG/GG"
+    if args.config == "cfg5":
+        name = "PhiMoE 16x(4096/6400)" if args.moe == "phimoe" else "Mixtral-8x22B 8x(6144/16384)"
+        return f"decode tokens/s, {name} MoE FFN layer top-2, expert-parallel, batch {args.batch}/GPU"
     if args.config == "cfg3":
         return ("prefill tokens/s, Mixtral-8x7B 32-layer MoE FFN stack, 512-token prompt with the "
                 "token-assignment split (n_g from solve_ng), then 128 decode steps")
@@ -106,7 +117,8 @@ def plan_rates(args, tokens_per_step):
     import paper_2411_15715_b200 as sp
 
     profile, source = load_profile(args.profile)
-    layer = sp.LayerSpec(args.model_dim, args.hidden_dim, n_gemms=args.top_k * 3, precision=sp.Precision.FP16)
+    hidden = getattr(args, "shard_hidden", args.hidden_dim)
+    layer = sp.LayerSpec(args.model_dim, hidden, n_gemms=args.top_k * 3, precision=sp.Precision.FP16)
     budget = args.budget_frac * layer.layer_bytes
     if args.config == "cfg1":
         return sp.SlicingRates(0.2, 0.3, 0.5), budget, "fixed 0.2/0.3/0.5 (BASELINE configs[0])", profile
@@ -225,10 +237,13 @@ def dist_env():
 
 
 def base_config(args, rates, global_batch, world):
-    return {"workload": f"{'mixtral-8x7b' if args.config == 'cfg2' else 'cfg1-1024x3584'}-moe-ffn-decode",
+    wl = {"cfg1": "cfg1-1024x3584-moe-ffn-decode", "cfg2": "mixtral-8x7b-moe-ffn-decode",
+          "cfg4": "llama2-70b-dense-ffn-decode-colsharded",
+          "cfg5": f"{'phimoe' if args.moe == 'phimoe' else 'mixtral-8x22b'}-moe-ffn-decode-ep"}.get(args.config, args.config)
+    return {"workload": wl,
             "model_dim": args.model_dim, "hidden_dim": args.hidden_dim, "experts": args.experts,
             "top_k": args.top_k, "batch_per_gpu": args.batch, "global_batch": global_batch,
-            "parallelism": f"ep{world}" if world > 1 else "single",
+            "parallelism": (f"col{world}" if args.config == "cfg4" else f"ep{world}") if world > 1 else "single",
             "rates": {"cc": rates.cc, "cg": rates.cg, "gg": rates.gg}}
 
 
@@ -251,13 +266,13 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def make_experts(args, rates, owned, device):
+def make_experts(args, rates, owned, device, hidden=None):
     """Random-init experts (HF layout) placed by `rates`."""
     import torch
 
     from paper_2411_15715_b200.sliced import SlicedFFN
 
-    M, H = args.model_dim, args.hidden_dim
+    M, H = args.model_dim, hidden or args.hidden_dim
     tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     experts = {}
     for e in owned:
@@ -289,11 +304,20 @@ def run_ours(args):
 
     B = args.batch
     global_batch = B * world
+    if args.config == "cfg4":
+        from paper_2411_15715_b200.expert_parallel import ColumnShardedFFN, column_shard
+
+        lo, hi = column_shard(args.hidden_dim, rank, world)
+        args.shard_hidden = hi - lo
     rates, budget, source, profile = plan_rates(args, B)
-    experts = make_experts(args, rates, local_experts(args.experts, rank, world), device)
     rng = np.random.default_rng(7)
-    router = rng.standard_normal((args.model_dim, args.experts))
-    moe = ExpertParallelMoE(experts, router, args.top_k, args.experts, out_dim=args.model_dim)
+    if args.config == "cfg4":
+        experts = make_experts(args, rates, [rank], device, hidden=hi - lo)
+        moe = ColumnShardedFFN(experts[rank])
+    else:
+        experts = make_experts(args, rates, local_experts(args.experts, rank, world), device)
+        router = rng.standard_normal((args.model_dim, args.experts))
+        moe = ExpertParallelMoE(experts, router, args.top_k, args.experts, out_dim=args.model_dim)
     pool = 64
     tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     xs_dev = [torch.from_numpy(rng.standard_normal((global_batch, args.model_dim)).astype(np.float32)).to(device, tdt)

@@ -123,3 +123,39 @@ class ExpertParallelMoE:
         return y
 
     __call__ = forward
+
+
+def column_shard(hidden: int, rank: int, world: int) -> tuple[int, int]:
+    """Hidden columns [lo, hi) owned by `rank` (BASELINE configs[3]: a dense FFN
+    column-sharded over G GPUs -- the same algebra as the CC/CG/GG split)."""
+    return hidden * rank // world, hidden * (rank + 1) // world
+
+
+class ColumnShardedFFN:
+    """Dense FFN whose hidden columns are split over the ranks; every rank runs
+    its own CC/CG/GG split of its shard (rates solved on LayerSpec(M, H/G)) and
+    one all-reduce sums the partial outputs."""
+
+    def __init__(self, shard, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.shard = shard  # SlicedFFN over this rank's columns
+
+    def forward(self, x):
+        import torch
+
+        y = self.shard(x)
+        if not isinstance(y, torch.Tensor):
+            y = torch.as_tensor(np.ascontiguousarray(y))
+        if self.world > 1:
+            if y.device.type == "cpu" and self.dist.get_backend(self.group) == "nccl":
+                yd = y.to(f"cuda:{torch.cuda.current_device()}")
+                self.dist.all_reduce(yd, group=self.group)
+                return yd.cpu()
+            self.dist.all_reduce(y, group=self.group)
+        return y
+
+    __call__ = forward

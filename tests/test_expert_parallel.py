@@ -88,3 +88,47 @@ def test_ownership_and_local_routing():
     # a rank whose experts nobody picked gets an empty plan
     unused = [e for e in range(8) if e not in ids]
     assert route_local(x, router, 2, unused) == []
+
+
+def _col_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_15715_b200.expert_parallel import ColumnShardedFFN, column_shard
+
+        rng = np.random.default_rng(21)
+        M, H, T = 32, 90, 5
+        w1, w3, w2 = rng.uniform(-1, 1, (M, H)), rng.uniform(-1, 1, (M, H)), rng.uniform(-1, 1, (H, M))
+        x = rng.uniform(-1, 1, (T, M))
+        lo, hi = column_shard(H, rank, world)
+
+        class OracleShard:  # stand-in for this rank's SlicedFFN (GPU path covered by -m gpu)
+            def __call__(self, xx):
+                return torch.from_numpy(orc.dense_forward(x, w1[:, lo:hi], w2[lo:hi], "silu", w3[:, lo:hi]))
+
+        y = ColumnShardedFFN(OracleShard())(torch.from_numpy(x))
+        out_q.put((rank, y.numpy(), (lo, hi)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_column_sharded_dense_ffn():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_col_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(21)
+    M, H, T = 32, 90, 5
+    w1, w3, w2 = rng.uniform(-1, 1, (M, H)), rng.uniform(-1, 1, (M, H)), rng.uniform(-1, 1, (H, M))
+    x = rng.uniform(-1, 1, (T, M))
+    ref = orc.dense_forward(x, w1, w2, "silu", w3)
+    shards = sorted(r[2] for r in res)
+    assert shards == [(0, 45), (45, 90)]
+    for _, y, _ in res:
+        np.testing.assert_allclose(y, ref, rtol=0, atol=1e-10)
