@@ -111,18 +111,33 @@ def load_profile(path):
     return costs.profile_from_dict(FALLBACK_DECODE), "fallback (b200_profile.FALLBACK_DECODE)"
 
 
+def expected_active(experts: int, top_k: int, batch: int) -> float:
+    """Expected distinct experts a batch of `batch` tokens touches with uniform top-k routing."""
+    return experts * (1.0 - (1.0 - top_k / experts) ** batch)
+
+
 def plan_rates(args, tokens_per_step):
     """greedy_assign under the budget picks r_GG, solve_rcg the best r_CG
-    (config 1 uses the fixed rates of BASELINE.json configs[0])."""
+    (config 1 uses the fixed rates of BASELINE.json configs[0]).
+
+    MoE decode is modelled the reference's way, n_gemms = active experts x 3
+    (PAPER.md:157), with the expected number of experts a batch activates and
+    the tokens each of them sees (hard part 6)."""
+    import math
+
     import paper_2411_15715_b200 as sp
 
     profile, source = load_profile(args.profile)
     hidden = getattr(args, "shard_hidden", args.hidden_dim)
-    layer = sp.LayerSpec(args.model_dim, hidden, n_gemms=args.top_k * 3, precision=sp.Precision.FP16)
+    e_act = min(expected_active(args.experts, args.top_k, tokens_per_step), args.experts) if args.experts > 1 \
+        else 1.0
+    n_gemms = max(args.top_k, round(e_act)) * 3
+    t_expert = max(1, math.ceil(tokens_per_step * args.top_k / max(e_act, 1.0)))
+    layer = sp.LayerSpec(args.model_dim, hidden, n_gemms=n_gemms, precision=sp.Precision.FP16)
     budget = args.budget_frac * layer.layer_bytes
     if args.config == "cfg1":
         return sp.SlicingRates(0.2, 0.3, 0.5), budget, "fixed 0.2/0.3/0.5 (BASELINE configs[0])", profile
-    wl = sp.Workload(tokens=tokens_per_step, phase=sp.Phase.GENERATION)
+    wl = sp.Workload(tokens=t_expert, phase=sp.Phase.GENERATION)
     mem = sp.greedy_assign(profile, [layer], wl, budget, n_steps=16)
     return sp.solve_rcg(profile, layer, wl, mem.per_layer_rgg[0]).rates, budget, source, profile
 

@@ -414,7 +414,14 @@ struct CallWs {
 };
 
 // ---- tensor-core (tcgen05) block path for many tokens -------------------------
-static const int g_tc_min_tokens = env_int("SP_TC_MIN_T", 16);
+// Tensor-core path as soon as the CUDA-core path would need a second token tile
+// (and so re-stream the weights); SP_TC_MIN_T overrides the threshold.
+static const int g_tc_min_tokens_env = env_int("SP_TC_MIN_T", 0);
+static int max_token_tile(int64_t M);
+static bool use_tc(const sp_layer* L, int64_t T) {
+  if (L->d.wdtype != SP_BF16) return false;
+  return g_tc_min_tokens_env > 0 ? T >= g_tc_min_tokens_env : T > max_token_tile(L->d.model_dim);
+}
 constexpr int kTcMaxSplits = 24;  // split-K output slices a resident tc block may use
 
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
@@ -606,7 +613,7 @@ static void set_tokens(FfnArgs& a, const int32_t* host_ids, int64_t T_e, int t0,
 static int run_block(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,
                      int64_t ldx, CallWs& w, const int32_t* host_ids, int64_t T_e, int t0, int T,
                      cudaStream_t s, int min_rows = g_min_rows_per_cta) {
-  if (L->d.wdtype == SP_BF16 && T >= g_tc_min_tokens && w.x_tc && w.a_tc)
+  if (use_tc(L, T) && w.x_tc && w.a_tc)
     return run_block_tc(C, L, b, x, xdtype, ldx, w, w.ids, T_e, t0, T, s, min_rows == g_min_rows_per_cta);
   const int grid = block_grid(C, b.rows, min_rows);
   const int tt_max = max_token_tile(L->d.model_dim);
@@ -803,13 +810,13 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int64_t Te = calls[c].tokens;
-    const bool tc_call = L->d.wdtype == SP_BF16 && Te >= g_tc_min_tokens;
+    const bool tc_call = use_tc(L, Te);
     ws_split[c] = tc_call ? kTcMaxSplits : 0;
     int64_t slices = block_grid(C, L->h_gg) + 1 + ws_split[c];  // + tc accumulation slice + tc splits
     for (int ci = 0; ci < int(L->chunks.size()); ++ci)
       if (ci >= L->n_cc_chunks || calls[c].n_g > 0) slices += block_grid(C, L->chunks[ci].rc, g_chunk_min_rows);
     o_part[c] = dalloc(size_t(slices) * Te * N * 4);
-    const bool tc = L->d.wdtype == SP_BF16 && Te >= g_tc_min_tokens;
+    const bool tc = tc_call;
     int64_t max_rows = L->h_gg;
     for (const Chunk& ch : L->chunks) max_rows = std::max(max_rows, ch.rc);
     ws_ld_a[c] = round_up(std::max<int64_t>(max_rows, 1), 64);
@@ -957,7 +964,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       const sp_layer* L = calls[c].layer;
       const int Te = int(calls[c].tokens);
       if (Te == 0 || L->h_gg <= 0) continue;
-      const bool tc = L->d.wdtype == SP_BF16 && Te >= g_tc_min_tokens;
+      const bool tc = use_tc(L, Te);
       const sp_layer* L0 = group.empty() ? L : calls[group[0]].layer;
       const bool same = L->d.wdtype == L0->d.wdtype && L->d.gated == L0->d.gated && L->d.act == L0->d.act;
       if (!tc && Te <= tt_max && same && int(group.size()) < kMaxGroup) {
