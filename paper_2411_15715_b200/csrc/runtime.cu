@@ -972,7 +972,9 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         continue;
       }
       BlockView b{static_cast<const char*>(L->gg), L->gg_w3_off, L->gg_w2_off, L->h_gg};
-      GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, double(L->gg_bytes) * ((Te + 3) / 4));
+      // weight bytes streamed: once on the tensor-core path, once per token tile otherwise
+      const double passes = tc ? 1.0 : double((Te + tt_max - 1) / tt_max);
+      GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, double(L->gg_bytes) * passes);
       SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, 0, Te, C->s_comp));
       span.end();
     }

@@ -133,7 +133,10 @@ def test_device_io_matches_host_io(sp, torch):
     ref = orc.dense_forward(orc.bf16_round(x.float().cpu().numpy()), orc.bf16_round(w1t.T),
                             orc.bf16_round(w2t.T), "silu", orc.bf16_round(w3t.T))
     assert orc.max_rel_error(y_dev.float().cpu().numpy(), ref) <= BF16_TOL
-    assert orc.max_rel_error(y_host, ref) <= 1e-4
+    # 5 tokens take the tensor-core path (bf16 hidden activations): bf16 bound
+    assert orc.max_rel_error(y_host, ref) <= BF16_TOL
+    # same arithmetic either way: device and host I/O differ only by the bf16 output cast
+    assert orc.max_rel_error(y_dev.float().cpu().numpy(), y_host) <= 4e-3
 
 
 def test_moe_top2_matches_oracle(sp, torch):
