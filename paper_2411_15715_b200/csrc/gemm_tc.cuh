@@ -61,6 +61,10 @@ struct GemmArgs {
   int64_t ldy;
   int split_slices;
   int64_t y_split_stride;
+  // up with ks > 1: split q stores fp32 pre-activations z[q][a][t][h] (ld = zld) and
+  // swiglu_reduce_kernel finishes (sum in split order, act, gate, bf16)
+  float* z;
+  int64_t zld;
   // split-K partials [tile][ks][NA][128][NT] fp32 and tickets [tile]
   float* partial;
   int* tickets;
@@ -232,7 +236,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(tmem_full, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
-    if (DOWN && g.split_slices) {
+    if (!DOWN && g.ks > 1) {
+#pragma unroll 1
+      for (int c = 0; c < NT; c += 16) {
+        uint32_t r[NA][16];
+#pragma unroll
+        for (int a = 0; a < NA; ++a) {
+          if (kb1 > kb0) {
+            tmem_ld16(lane_addr + uint32_t(a * NT + c), r[a]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[a][e] = 0u;
+          }
+        }
+        if (m >= g.rows) continue;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int t = t0 + c + e;
+          if (t >= g.T) break;
+#pragma unroll
+          for (int a = 0; a < NA; ++a)
+            g.z[((int64_t(ks_id) * NA + a) * g.T + t) * g.zld + m] = __uint_as_float(r[a][e]);
+        }
+      }
+    } else if (DOWN && g.split_slices) {
       float* ys = g.y + int64_t(ks_id) * g.y_split_stride;
 #pragma unroll 1
       for (int c = 0; c < NT; c += 16) {
@@ -366,6 +393,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
   }
+}
+
+// a[t, h] = act(sum_q z[q][0][t][h]) [* sum_q z[q][1][t][h]], splits summed in order
+__global__ void swiglu_reduce_kernel(const float* __restrict__ z, int ks, int na, int T, int R, int64_t zld,
+                                     int act, __nv_bfloat16* __restrict__ a_out, int64_t lda) {
+  const int t = blockIdx.y;
+  const int h = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (h >= R) return;
+  const int64_t plane = int64_t(T) * zld;
+  float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
+  for (int q = 0; q < ks; ++q) {
+    const float* base = z + (int64_t(q) * na * T + t) * zld + h;
+    const float4 v0 = __ldcg(reinterpret_cast<const float4*>(base));
+    s0.x += v0.x; s0.y += v0.y; s0.z += v0.z; s0.w += v0.w;
+    if (na == 2) {
+      const float4 v1 = __ldcg(reinterpret_cast<const float4*>(base + plane));
+      s1.x += v1.x; s1.y += v1.y; s1.z += v1.z; s1.w += v1.w;
+    }
+  }
+  float o[4] = {act_fn(act, s0.x), act_fn(act, s0.y), act_fn(act, s0.z), act_fn(act, s0.w)};
+  if (na == 2) {
+    o[0] *= s1.x; o[1] *= s1.y; o[2] *= s1.z; o[3] *= s1.w;
+  }
+  __nv_bfloat16* dst = a_out + int64_t(t) * lda + h;
+  for (int e = 0; e < 4 && h + e < R; ++e) dst[e] = __float2bfloat16_rn(o[e]);
 }
 
 // gather x rows (any dtype) into a contiguous bf16 [T, ldo] buffer

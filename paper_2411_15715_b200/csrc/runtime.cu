@@ -140,6 +140,7 @@ struct Context {
   PinnedBuf xroute;  // x read back for the MoE router (and reused by the CC blocks)
   DevBuf tc_partial;  // split-K partial tiles of the tensor-core GEMMs
   DevBuf tc_tickets;  // per-tile split tickets (zero, re-armed by the last split)
+  DevBuf tc_z;        // up-GEMM split partials of the pre-activations
   std::vector<float> hscratch;
   std::unique_ptr<ThreadPool> pool;
   int host_threads = 1;
@@ -541,10 +542,23 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
   up.ks = split_k(up.m_tiles * t_tiles, int(M), target);
   up.a_out = w.a_tc;
   up.lda = w.ld_a;
+  const int na = L->d.gated ? 2 : 1;
+  if (up.ks > 1) {
+    // split partials of the pre-activations, finished by swiglu_reduce_kernel
+    up.zld = round_up(R, 4);
+    SP_TRY(C->tc_z.ensure(size_t(up.ks) * na * T * up.zld * 4));
+    up.z = static_cast<float*>(C->tc_z.p);
+  }
   if (L->d.gated)
     SP_TRY((launch_gemm<2, false>(C, nt, tw1, tw3, tx, up, s)));
   else
     SP_TRY((launch_gemm<1, false>(C, nt, tw1, tw1, tx, up, s)));
+  if (up.ks > 1) {
+    dim3 grid(unsigned((R / 4 + 127) / 128 + 1), unsigned(T));
+    tc::swiglu_reduce_kernel<<<grid, 128, 0, s>>>(up.z, up.ks, na, T, int(R), up.zld, L->d.act, w.a_tc, w.ld_a);
+    SP_CUDA(cudaGetLastError());
+    ++C->launches;
+  }
   SP_TRY(make_tmap(&tw2, b.base + b.w2_off, N, R, L->ldn * 2, 64, tc::BK));
   SP_TRY(make_tmap(&ta, w.a_tc, R, T, w.ld_a * 2, tc::BK, nt));
   tc::GemmArgs dn{};
