@@ -15,6 +15,17 @@ runtime executes on, through the runtime's own code paths:
   stream trace spans) over chunk sizes 0.8 - 31 MB.
 * ``launch``        -- host enqueue time per kernel launch of a forward.
 
+The CC threads and the copy engine read the same host DRAM at the same time
+in every sliced step (the CC block runs while the CG chunks stream), and the
+GG kernels run while the copy engine writes the HBM ring (measured: the
+copies cost a GG launch ~25 % of its HBM rate, scripts/probe_gg.py).  By
+default (``--load concurrent``) every rate is therefore sampled under the load
+the step puts next to it: decode CC blocks and chunk copies come from real
+sliced decode steps (``insitu_samples``), GG blocks run under background
+host -> HBM copies, prompt-phase CC blocks under background copies and
+prompt-phase copies under a background CC block.  ``--load isolated`` samples
+each rate alone (the round-1 method).
+
 ``python -m paper_2411_15715_b200.b200_profile --out profiles/`` writes the
 CSV and the fitted profile JSON (per phase: the GPU term is far from linear in
 T across decode and prefill, SURVEY.md section 7 hard part 3).
@@ -24,6 +35,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import threading
 import time
 from pathlib import Path
 
@@ -46,6 +58,65 @@ FALLBACK_DECODE = {
         }
     },
 }
+
+
+class BackgroundCopy:
+    """Keeps pinned host -> HBM copies in flight on a side stream (the CG
+    streamer's host-DRAM load) while the block runs."""
+
+    def __init__(self, torch, nbytes=64 << 20):
+        self.torch = torch
+        self.host = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        self.dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        self.stream = torch.cuda.Stream()
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        torch = self.torch
+        while not self.stop.is_set():
+            with torch.cuda.stream(self.stream):
+                for _ in range(4):
+                    self.dev.copy_(self.host, non_blocking=True)
+            self.stream.synchronize()
+
+    def __enter__(self):
+        self.th.start()
+        time.sleep(0.05)
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        self.th.join()
+
+
+class BackgroundCC:
+    """Keeps a 150 MB CC block running on the host threads (the CC block's
+    host-DRAM load) while the chunk copies are sampled."""
+
+    def __init__(self, model_dim=4096, hidden=6144, seed=5):
+        from .sliced import NativeLayer
+
+        rng = np.random.default_rng(seed)
+        w = rng.standard_normal((hidden, model_dim), dtype=np.float32) / 64
+        self.lay = NativeLayer(w, w, hidden, hidden, "silu", w, dtype="bf16")
+        self.x = rng.standard_normal((1, model_dim))
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self.stop.is_set():
+            self.lay.cc_forward_host(self.x)
+
+    def __enter__(self):
+        self.th.start()
+        time.sleep(0.05)
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        self.th.join()
+        self.lay.release()
 
 
 def _flush_l2(torch, scratch):
@@ -132,6 +203,47 @@ def c2g_samples(torch, chunk_rows=(32, 64, 128, 320, 640, 1280), reps=3, model_d
     return out
 
 
+def insitu_samples(torch, cc_rates=(0.1, 0.2, 0.3, 0.4), r_gg=0.5, model_dim=4096, hidden=14336,
+                   experts=2, reps=6, seed=11):
+    """CPU GEMM and chunk-copy samples taken from real sliced decode steps.
+
+    For each CC rate, `experts` SwiGLU experts are placed with rates
+    (cc, 1 - r_gg - cc, r_gg) and run as one batched decode forward (the
+    top-2 MoE step): the CC blocks (host threads) and the CG chunk copies
+    (copy engine) then share host DRAM exactly as they do in production.
+    Every CC block's host span gives one ``cpu_gemm_fp16`` sample (n = T*M*b1
+    per GEMM, span / 3) and every chunk copy one ``c2g`` sample."""
+    from .sliced import CallSpec, NativeLayer, forward_calls
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    mk = lambda *s: (torch.randn(*s, device="cuda", generator=g) / 64).to(torch.bfloat16).cpu()  # noqa: E731
+    weights = [(mk(hidden, model_dim), mk(hidden, model_dim), mk(hidden, model_dim)) for _ in range(experts)]
+    x = torch.randn(1, model_dim, device="cuda").to(torch.bfloat16)
+    out = []
+    for cc in cc_rates:
+        b1 = int(np.floor(cc * hidden))
+        b2 = int(np.floor((1.0 - r_gg) * hidden))
+        lays = [NativeLayer(w1t, w2, b1, b2, "silu", w3t, dtype="bf16") for (w1t, w3t, w2) in weights]
+        for r in range(reps + 2):
+            torch.cuda.synchronize()
+            nat.trace_enable(True)
+            forward_calls([CallSpec(l) for l in lays], x)
+            torch.cuda.synchronize()
+            spans = nat.trace_fetch()
+            nat.trace_enable(False)
+            if r < 2:
+                continue
+            for s_ in spans:
+                dt = s_["end_s"] - s_["start_s"]
+                if s_["kind"] == "cc":
+                    out.append(ProfileSample(OpClass.CPU_GEMM, float(model_dim) * b1, dt / 3.0, Precision.FP16))
+                elif s_["kind"] == "copy":
+                    out.append(ProfileSample(OpClass.C2G, float(s_["bytes"]), dt))
+        for l in lays:
+            l.release()
+    return out
+
+
 def launch_samples(torch, reps=20):
     from .sliced import CallSpec, NativeLayer, forward_calls
 
@@ -154,7 +266,7 @@ def launch_samples(torch, reps=20):
     return out
 
 
-def measure(phase: str = "decode", quick: bool = False) -> list[ProfileSample]:
+def measure(phase: str = "decode", quick: bool = False, load: str = "concurrent") -> list[ProfileSample]:
     """decode: T = 1 everywhere.  prompt: the GPU GEMM at T = 128 tokens (an
     expert's share of a 512-token top-2 prompt, tensor-core path) and the host
     GEMM at T = 32 -- one profile per phase, because t_G = alpha + T*M*H*beta
@@ -167,9 +279,23 @@ def measure(phase: str = "decode", quick: bool = False) -> list[ProfileSample]:
     cpu_widths = [128, 256, 512, 1024, 2048, 4096] if phase == "decode" else [64, 128, 256, 512]
     if quick:
         widths, cpu_widths = [1024, 4096, 14336], cpu_widths[:3]
-    samples = gpu_gemm_samples(torch, gpu_tokens, widths, reps=3 if quick else 5)
-    samples += cpu_gemm_samples(cpu_tokens, cpu_widths, reps=2 if quick else 4)
-    samples += c2g_samples(torch)
+    if load == "concurrent":
+        # every rate under the load the step puts next to it: GG kernels while
+        # the copy engine writes the ring, CC blocks and chunk copies from
+        # real sliced steps (decode), copies under a running CC block (prompt)
+        with BackgroundCopy(torch):
+            samples = gpu_gemm_samples(torch, gpu_tokens, widths, reps=3 if quick else 5)
+        if phase == "decode":
+            samples += insitu_samples(torch, reps=3 if quick else 6)
+        else:
+            with BackgroundCopy(torch):
+                samples += cpu_gemm_samples(cpu_tokens, cpu_widths, reps=2 if quick else 4)
+            with BackgroundCC():
+                samples += c2g_samples(torch)
+    else:
+        samples = gpu_gemm_samples(torch, gpu_tokens, widths, reps=3 if quick else 5)
+        samples += cpu_gemm_samples(cpu_tokens, cpu_widths, reps=2 if quick else 4)
+        samples += c2g_samples(torch)
     samples += launch_samples(torch)
     return samples
 
@@ -179,12 +305,14 @@ def main(argv=None) -> None:
     ap.add_argument("--out", default="profiles")
     ap.add_argument("--phase", default="decode", choices=["decode", "prompt"])
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--load", default="concurrent", choices=["concurrent", "isolated"],
+                    help="sample the host-side rates under each other's host-DRAM load (default) or alone")
     args = ap.parse_args(argv)
     out = Path(args.out)
     out.mkdir(parents=True, exist_ok=True)
-    samples = measure(args.phase, args.quick)
+    samples = measure(args.phase, args.quick, args.load)
     write_samples_csv(samples, out / f"b200_samples_{args.phase}.csv")
-    prof, warns = fit_profile(samples, f"b200-{args.phase}")
+    prof, warns = fit_profile(samples, f"b200-{args.phase}" + ("" if args.load == "concurrent" else "-isolated"))
     (out / f"b200_{args.phase}.json").write_bytes(save_profile(prof))
     g = prof.gemm[Precision.FP16]
     summary = {

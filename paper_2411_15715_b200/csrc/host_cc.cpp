@@ -6,14 +6,42 @@
 #include <string.h>
 
 #include <algorithm>
+#include <pthread.h>
+#include <sched.h>
+#include <stdlib.h>
 
 namespace sp {
+
+// Software prefetch distance (bytes ahead on each weight stream; 0 = off).
+// Consecutive hidden units' rows are contiguous inside a chunk, so "ahead" runs
+// into the next row: the L2 streamer stops at every 4 KB page, this does not.
+static int env_or(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+static const int g_cc_pf = env_or("SP_CC_PREFETCH", 0);
 
 // ---------------------------------------------------------------------------
 // thread pool: persistent workers, the caller participates as tid 0
 
 ThreadPool::ThreadPool(int n_threads) : n_(std::max(1, n_threads)) {
   for (int t = 1; t < n_; ++t) threads_.emplace_back([this, t] { worker(t); });
+  // SP_PIN_THREADS=1: worker t on the t-th CPU of the process affinity mask
+  if (env_or("SP_PIN_THREADS", 0)) {
+    cpu_set_t allowed;
+    CPU_ZERO(&allowed);
+    if (sched_getaffinity(0, sizeof(allowed), &allowed) == 0) {
+      std::vector<int> cpus;
+      for (int c = 0; c < CPU_SETSIZE; ++c)
+        if (CPU_ISSET(c, &allowed)) cpus.push_back(c);
+      for (int t = 1; t < n_ && !cpus.empty(); ++t) {
+        cpu_set_t one;
+        CPU_ZERO(&one);
+        CPU_SET(cpus[size_t(t) % cpus.size()], &one);
+        pthread_setaffinity_np(threads_[size_t(t - 1)].native_handle(), sizeof(one), &one);
+      }
+    }
+  }
 }
 
 ThreadPool::~ThreadPool() {
@@ -92,7 +120,11 @@ __attribute__((target("avx512f,avx512bw,fma"))) static void dot_tile_avx512(
   __m512 acc[NR][NT];
   for (int r = 0; r < NR; ++r)
     for (int t = 0; t < NT; ++t) acc[r][t] = _mm512_setzero_ps();
+  constexpr int64_t kEsz = WD == 1 ? 2 : 4;
   for (int64_t k = 0; k < k16; k += 16) {
+    if (g_cc_pf && ((k * kEsz) & 63) == 0)
+      for (int r = 0; r < NR; ++r)
+        _mm_prefetch(static_cast<const char*>(rows[r]) + k * kEsz + g_cc_pf, _MM_HINT_T0);
     __m512 w[NR];
     for (int r = 0; r < NR; ++r) w[r] = load16<WD>(rows[r], k);
     for (int t = 0; t < NT; ++t) {
@@ -172,7 +204,11 @@ static inline int64_t round16(int64_t v) { return (v + 15) / 16 * 16; }
 template <int WD, int NR>
 __attribute__((target("avx512f,avx512bw,fma"))) static void axpy_rows_avx512(
     const void* const* rows, const float* a /*[NR][T]*/, int64_t T, float* ybuf, int64_t ldy, int64_t n16) {
+  constexpr int64_t kEsz = WD == 1 ? 2 : 4;
   for (int64_t n = 0; n < n16; n += 16) {
+    if (g_cc_pf && ((n * kEsz) & 63) == 0)
+      for (int r = 0; r < NR; ++r)
+        _mm_prefetch(static_cast<const char*>(rows[r]) + n * kEsz + NR * g_cc_pf, _MM_HINT_T0);
     __m512 w[NR];
     for (int r = 0; r < NR; ++r) w[r] = load16<WD>(rows[r], n);
     for (int64_t t = 0; t < T; ++t) {
@@ -232,45 +268,64 @@ void cc_forward(const CCProblem& p, ThreadPool& pool, int threads) {
   for (int c = 0; c < p.n_chunks; ++c)
     for (int64_t r = 0; r < p.chunks[c].rc; ++r) chunk_of[size_t(p.chunks[c].r0 + r)] = c;
 
-  // per-thread partial outputs [n_thr][T][n16]
-  std::vector<float> ybufs(size_t(n_thr) * T * n16, 0.f);
+  // Hidden rows are processed in blocks claimed dynamically (an atomic
+  // cursor), so a preempted or slow thread does not hold up the block: with
+  // 16 threads on a shared 16-vCPU host the static split's tail was the CC
+  // block's largest jitter.  Each row block accumulates into its own partial
+  // slice and the slices are summed in block order -- the result does not
+  // depend on which thread ran which block (deterministic).
+  const int64_t slice = T * n16;
+  const int64_t budget = (int64_t(8) << 20) / (slice * 4);  // partial slices within 8 MB
+  int64_t nb = std::min<int64_t>(p.b1, std::max<int64_t>(n_thr, std::min<int64_t>(budget, 8 * n_thr)));
+  nb = std::max<int64_t>(1, nb);
+  std::vector<float> ybufs(size_t(nb) * slice);
+  std::atomic<int64_t> cursor{0};
 
-  auto rows_pass = [&](int tid, int n) {
-    const int64_t h0 = p.b1 * tid / n, h1 = p.b1 * (tid + 1) / n;
-    float* ybuf = ybufs.data() + size_t(tid) * T * n16;
+  auto rows_pass = [&](int, int) {
     std::vector<float> s(size_t(2 * T)), a(size_t(4 * T));
     const void* w2rows[4];
-    int pend = 0;
-    for (int64_t h = h0; h < h1; ++h) {
-      const HostChunk& c = p.chunks[chunk_of[size_t(h)]];
-      const int64_t off1 = (h - c.r0) * p.ldm * int64_t(esz);
-      const void* rows[2] = {static_cast<const char*>(c.w1t) + off1,
-                             p.gated ? static_cast<const char*>(c.w3t) + off1 : nullptr};
-      if (p.gated) {
-        dot_rows<2>(rows, k_up, p.x, p.ldx, T, wd, s.data());
-        for (int64_t t = 0; t < T; ++t) a[pend * T + t] = act_host(p.act, s[t]) * s[T + t];
-      } else {
-        dot_rows<1>(rows, k_up, p.x, p.ldx, T, wd, s.data());
-        for (int64_t t = 0; t < T; ++t) a[pend * T + t] = act_host(p.act, s[t]);
-      }
-      w2rows[pend++] = static_cast<const char*>(c.w2) + (h - c.r0) * p.ldn * int64_t(esz);
-      if (pend == 4 || h + 1 == h1) {
-        axpy_rows(w2rows, pend, a.data(), T, ybuf, n16, n16, wd);
-        pend = 0;
+    for (;;) {
+      const int64_t blk = cursor.fetch_add(1, std::memory_order_relaxed);
+      if (blk >= nb) break;
+      const int64_t h0 = p.b1 * blk / nb, h1 = p.b1 * (blk + 1) / nb;
+      float* ybuf = ybufs.data() + size_t(blk) * slice;
+      std::fill(ybuf, ybuf + slice, 0.f);
+      int pend = 0;
+      for (int64_t h = h0; h < h1; ++h) {
+        const HostChunk& c = p.chunks[chunk_of[size_t(h)]];
+        const int64_t off1 = (h - c.r0) * p.ldm * int64_t(esz);
+        const void* rows[2] = {static_cast<const char*>(c.w1t) + off1,
+                               p.gated ? static_cast<const char*>(c.w3t) + off1 : nullptr};
+        if (p.gated) {
+          dot_rows<2>(rows, k_up, p.x, p.ldx, T, wd, s.data());
+          for (int64_t t = 0; t < T; ++t) a[pend * T + t] = act_host(p.act, s[t]) * s[T + t];
+        } else {
+          dot_rows<1>(rows, k_up, p.x, p.ldx, T, wd, s.data());
+          for (int64_t t = 0; t < T; ++t) a[pend * T + t] = act_host(p.act, s[t]);
+        }
+        w2rows[pend++] = static_cast<const char*>(c.w2) + (h - c.r0) * p.ldn * int64_t(esz);
+        if (pend == 4 || h + 1 == h1) {
+          axpy_rows(w2rows, pend, a.data(), T, ybuf, n16, n16, wd);
+          pend = 0;
+        }
       }
     }
   };
   pool.run(n_thr, rows_pass);
 
   auto reduce = [&](int tid, int n) {
-    const int64_t c0 = (n16 / 16) * tid / n * 16, c1 = (n16 / 16) * (tid + 1) / n * 16;
-    for (int64_t t = 0; t < T; ++t)
-      for (int64_t col = c0; col < c1; ++col) {
-        if (col >= p.N) break;
-        float v = 0.f;
-        for (int i = 0; i < n_thr; ++i) v += ybufs[(size_t(i) * T + t) * n16 + col];
-        p.y[t * p.N + col] = v;
+    const int64_t c0 = (n16 / 16) * tid / n * 16;
+    const int64_t c1 = std::min<int64_t>((n16 / 16) * (tid + 1) / n * 16, p.N);
+    if (c1 <= c0) return;
+    std::vector<float> acc(size_t(c1 - c0));
+    for (int64_t t = 0; t < T; ++t) {
+      std::fill(acc.begin(), acc.end(), 0.f);
+      for (int64_t i = 0; i < nb; ++i) {  // block order: deterministic
+        const float* src = ybufs.data() + size_t(i) * slice + t * n16;
+        for (int64_t col = c0; col < c1; ++col) acc[size_t(col - c0)] += src[col];
       }
+      std::copy(acc.begin(), acc.end(), p.y + t * p.N + c0);
+    }
   };
   pool.run(threads, reduce);
 }

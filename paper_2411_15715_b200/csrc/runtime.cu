@@ -13,6 +13,7 @@
 #include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <cmath>
@@ -151,7 +152,8 @@ struct Context {
   std::mutex cc_mu;
   std::condition_variable cc_cv;
   std::function<int()> cc_job;
-  bool cc_pending = false, cc_stop = false;
+  std::function<int()> cc_tail;  // work to run after the CC block (see cc_join_with_tail)
+  bool cc_pending = false, cc_stop = false, cc_done = false;
   int cc_status = 0;
   std::string cc_error;
   std::mutex trace_mu;  // spans come from the calling thread and the coordinator
@@ -208,6 +210,7 @@ struct sp_layer {
   size_t host_bytes = 0, cc_bytes = 0, cg_bytes = 0;
   std::vector<sp::Chunk> chunks;
   bool host_only = false;
+  size_t host_map_bytes = 0;  // > 0: host region is an mmap'd (THP) range registered with CUDA
   int n_cc_chunks = 0;
   size_t max_chunk_bytes = 0;
 };
@@ -220,6 +223,10 @@ static void copy_rows(char* dst, int64_t ld, const char* src, int64_t cols, int6
   for (int64_t r = 0; r < n; ++r)
     memcpy(dst + size_t(r) * ld * esz, src + size_t(r0 + r) * cols * esz, size_t(cols) * esz);
 }
+
+static int env_int(const char* name, int dflt);
+// SP_HUGEPAGES=1: CC/CG host region on 2 MB transparent huge pages (mmap + cudaHostRegister)
+static const bool g_hugepages = env_int("SP_HUGEPAGES", 0) != 0;
 
 static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void* w2) {
   const sp_layer_desc& d = L->d;
@@ -286,6 +293,21 @@ static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void*
     if (L->host_only) {
       L->host = aligned_alloc(4096, off);
       if (!L->host) return fail(SP_ERR_NOMEM, "aligned_alloc(%zu) failed", off);
+    } else if (g_hugepages) {
+      // 2 MB transparent huge pages: the CC threads' streams cross far fewer TLB
+      // entries; the range is then page-locked for the copy engine.
+      const size_t map = size_t(round_up(int64_t(off), int64_t(2) << 20));
+      void* p = mmap(nullptr, map, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+      if (p == MAP_FAILED) return fail(SP_ERR_NOMEM, "mmap(%zu) for the CC/CG blocks failed", map);
+      madvise(p, map, MADV_HUGEPAGE);
+      memset(p, 0, map);
+      if (cudaHostRegister(p, map, cudaHostRegisterDefault) != cudaSuccess) {
+        cudaGetLastError();
+        munmap(p, map);
+        return fail(SP_ERR_NOMEM, "cudaHostRegister(%zu) for the CC/CG blocks failed", map);
+      }
+      L->host = p;
+      L->host_map_bytes = map;
     } else if (cudaHostAlloc(&L->host, off, cudaHostAllocDefault) != cudaSuccess) {
       cudaGetLastError();
       return fail(SP_ERR_NOMEM, "cudaHostAlloc(%zu) for the CC/CG blocks failed", off);
@@ -737,9 +759,19 @@ static void cc_coordinator(Context* C) {
     std::function<int()> job = std::move(C->cc_job);
     C->cc_job = nullptr;
     lk.unlock();
-    const int st = job();
-    const std::string err = st == SP_OK ? std::string() : g_err;
+    int st = job();
+    std::string err = st == SP_OK ? std::string() : g_err;
     lk.lock();
+    C->cc_done = true;
+    if (st == SP_OK && C->cc_tail) {
+      // the launching thread finished enqueueing first: run its tail here
+      std::function<int()> tail = std::move(C->cc_tail);
+      C->cc_tail = nullptr;
+      lk.unlock();
+      st = tail();
+      if (st != SP_OK) err = g_err;
+      lk.lock();
+    }
     C->cc_status = st;
     C->cc_error = err;
     C->cc_pending = false;
@@ -750,17 +782,32 @@ static void cc_coordinator(Context* C) {
 static void cc_submit(Context* C, std::function<int()> job) {
   std::lock_guard<std::mutex> g(C->cc_mu);
   C->cc_job = std::move(job);
+  C->cc_tail = nullptr;
+  C->cc_done = false;
   C->cc_pending = true;
   C->cc_status = SP_OK;
   C->cc_cv.notify_all();
 }
 
-static int cc_wait(Context* C) {
+// Join the CC block; `tail` (the work that needs its result) runs on the
+// coordinator if the block is still running, else here.
+static int cc_join_with_tail(Context* C, const std::function<int()>& tail) {
   std::unique_lock<std::mutex> lk(C->cc_mu);
+  if (!C->cc_done) {
+    C->cc_tail = tail;
+    C->cc_cv.wait(lk, [&] { return !C->cc_pending; });
+    if (C->cc_status != SP_OK) return fail(C->cc_status, "%s", C->cc_error.c_str());
+    if (!C->cc_tail) return SP_OK;  // ran on the coordinator
+    C->cc_tail = nullptr;
+    lk.unlock();
+    return tail();
+  }
   C->cc_cv.wait(lk, [&] { return !C->cc_pending; });
   if (C->cc_status != SP_OK) return fail(C->cc_status, "%s", C->cc_error.c_str());
-  return SP_OK;
+  lk.unlock();
+  return tail();
 }
+
 
 // ---------------------------------------------------------------------------
 // forward
@@ -880,6 +927,40 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   SP_CUDA(cudaEventRecord(C->ev_user, user));
   SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_user, 0));
 
+  // ---- CG chunks (and CC chunks for the n_g diverted rows): the copy stream
+  // is the step's bottleneck, so the first ring slots' copies are enqueued
+  // before anything else; each later copy right after the kernel that frees its slot.
+  struct StreamItem {
+    int c;
+    int ci;
+    int slot;
+  };
+  std::vector<StreamItem> items;
+  for (int c = 0; c < n_calls; ++c) {
+    const sp_layer* L = calls[c].layer;
+    if (calls[c].tokens == 0) continue;
+    for (int ci = 0; ci < int(L->chunks.size()); ++ci)
+      if (ci >= L->n_cc_chunks || calls[c].n_g > 0) items.push_back(StreamItem{c, ci, -1});
+  }
+  size_t next_copy = 0;
+  auto enqueue_copy = [&]() -> int {
+    StreamItem& it = items[next_copy++];
+    const sp_layer* L = calls[it.c].layer;
+    const Chunk& ch = L->chunks[size_t(it.ci)];
+    it.slot = C->ring_next;
+    C->ring_next = (C->ring_next + 1) % kRingSlots;
+    SP_CUDA(cudaStreamWaitEvent(C->s_copy, C->ev_free[it.slot], 0));
+    {
+      GpuSpan span(C, C->s_copy, 1, SP_TRACE_COPY, double(ch.bytes));
+      SP_CUDA(cudaMemcpyAsync(C->ring[it.slot].p, static_cast<const char*>(L->host) + ch.off, ch.bytes,
+                              cudaMemcpyHostToDevice, C->s_copy));
+      span.end();
+    }
+    C->h2d_bytes += ch.bytes;
+    SP_CUDA(cudaEventRecord(C->ev_copied[it.slot], C->s_copy));
+    return SP_OK;
+  };
+
   // ---- plan metadata (token ids, gates) ----
   {
     char* m = hp + p_meta;
@@ -924,6 +1005,9 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
                             C->s_comp));
   }
 
+  // the first ring slots' copies go right behind the (tiny) metadata copies
+  while (next_copy < items.size() && next_copy < size_t(kRingSlots)) SP_TRY(enqueue_copy());
+
   // ---- x: device copy for the GPU, host copy for the CC threads ----
   bool need_cc = false;
   for (int c = 0; c < n_calls; ++c)
@@ -937,8 +1021,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     x_dev = dws + o_xdev;
     x_host = x;
   } else if (need_cc && x_host_ready) {
-    x_host = x_host_ready;  // already read back by the caller (sp_moe_forward)
-    SP_CUDA(cudaEventRecord(C->ev_x, C->s_comp));
+    x_host = x_host_ready;  // already read back by the caller (sp_moe_forward): no GPU wait
   } else if (need_cc) {
     SP_CUDA(cudaMemcpyAsync(hp + p_x, x, size_t(T) * M * xel, cudaMemcpyDeviceToHost, C->s_comp));
     SP_CUDA(cudaEventRecord(C->ev_x, C->s_comp));
@@ -947,8 +1030,9 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
 
   // ---- CC block: submitted to the coordinator now, runs while we enqueue ----
   const bool cc_async = need_cc && !(flags & SP_NO_CC_THREADS);
+  const bool x_on_host_now = host_io || x_host_ready;
   auto cc_work = [=]() -> int {
-    if (!host_io) {
+    if (!x_on_host_now) {
       const cudaError_t e = cudaEventSynchronize(C->ev_x);
       if (e != cudaSuccess) return fail(SP_ERR_CUDA, "x copy for the CC block: %s", cudaGetErrorString(e));
     }
@@ -1019,67 +1103,52 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         ws[c].S += nc;
       }
       const int tt = te_max <= 1 ? 1 : te_max <= 2 ? 2 : 4;
+      // The GG launch is off the critical path (the copy stream paces the step):
+      // it is queued behind the first chunk copy, so the GPU starts it from a
+      // full queue -- no host-enqueue bubble inside its span -- and it still
+      // ends long before the last chunk kernel needs the stream.
+      if (!items.empty()) SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_copied[items[0].slot], 0));
       GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, bytes);
       SP_TRY(launch_group(C, calls[group[0]].layer, tt, g, cta, C->s_comp));
       span.end();
     }
   }
 
-  // ---- CG chunks (and CC chunks for the n_g diverted rows) through the ring ----
-  for (int c = 0; c < n_calls; ++c) {
+  // ---- chunk kernels, in copy order, each followed by the copy its slot frees ----
+  for (size_t i = 0; i < items.size(); ++i) {
+    const StreamItem it = items[i];
+    const int c = it.c;
     const sp_layer* L = calls[c].layer;
     const int Te = int(calls[c].tokens);
     const int ng = int(calls[c].n_g);
-    if (Te == 0) continue;
-    for (size_t ci = 0; ci < L->chunks.size(); ++ci) {
-      const Chunk& ch = L->chunks[ci];
-      const bool is_cc = int(ci) < L->n_cc_chunks;
-      if (is_cc && ng == 0) continue;
-      const int slot = C->ring_next;
-      C->ring_next = (C->ring_next + 1) % kRingSlots;
-      SP_CUDA(cudaStreamWaitEvent(C->s_copy, C->ev_free[slot], 0));
-      {
-        GpuSpan span(C, C->s_copy, 1, SP_TRACE_COPY, double(ch.bytes));
-        SP_CUDA(cudaMemcpyAsync(C->ring[slot].p, static_cast<const char*>(L->host) + ch.off,
-                                ch.bytes, cudaMemcpyHostToDevice, C->s_copy));
-        span.end();
-      }
-      C->h2d_bytes += ch.bytes;
-      SP_CUDA(cudaEventRecord(C->ev_copied[slot], C->s_copy));
-      SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_copied[slot], 0));
-      BlockView b{static_cast<const char*>(C->ring[slot].p), ch.w3_off, ch.w2_off, ch.rc};
-      const int t0 = is_cc ? Te - ng : 0;
-      if (t0 > 0) {
-        // a cg_prime block writes only rows [t0, Te) of its slices; the reducer sums every row
-        const size_t slice = size_t(Te) * N * 4;
-        SP_CUDA(cudaMemsetAsync(ws[c].part + size_t(ws[c].S) * Te * N, 0,
-                                slice * block_grid(C, ch.rc, g_chunk_min_rows), C->s_comp));
-      }
-      {
-        GpuSpan span(C, C->s_comp, 2, is_cc ? SP_TRACE_CG_PRIME : SP_TRACE_CG, double(ch.bytes));
-        SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, t0, Te - t0, C->s_comp,
-                         g_chunk_min_rows));
-        span.end();
-      }
-      SP_CUDA(cudaEventRecord(C->ev_free[slot], C->s_comp));
+    const Chunk& ch = L->chunks[size_t(it.ci)];
+    const bool is_cc = it.ci < L->n_cc_chunks;
+    SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_copied[it.slot], 0));
+    BlockView b{static_cast<const char*>(C->ring[it.slot].p), ch.w3_off, ch.w2_off, ch.rc};
+    const int t0 = is_cc ? Te - ng : 0;
+    if (t0 > 0) {
+      // a cg_prime block writes only rows [t0, Te) of its slices; the reducer sums every row
+      const size_t slice = size_t(Te) * N * 4;
+      SP_CUDA(cudaMemsetAsync(ws[c].part + size_t(ws[c].S) * Te * N, 0,
+                              slice * block_grid(C, ch.rc, g_chunk_min_rows), C->s_comp));
     }
+    {
+      GpuSpan span(C, C->s_comp, 2, is_cc ? SP_TRACE_CG_PRIME : SP_TRACE_CG, double(ch.bytes));
+      SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, t0, Te - t0, C->s_comp,
+                       g_chunk_min_rows));
+      span.end();
+    }
+    SP_CUDA(cudaEventRecord(C->ev_free[it.slot], C->s_comp));
+    if (next_copy < items.size()) SP_TRY(enqueue_copy());
   }
 
-  // ---- join the CC block, ship its partials ----
   host_span(C, 0, SP_TRACE_LAUNCH, t_call, now_s(), 0.0);
-  if (need_cc) {
-    SP_TRY(cc_async ? cc_wait(C) : cc_work());
-    for (int c = 0; c < n_calls; ++c) {
-      const int64_t Tcc = calls[c].tokens - calls[c].n_g;
-      if (calls[c].layer->d.b1 <= 0 || Tcc <= 0) continue;
-      SP_CUDA(cudaMemcpyAsync(ws[c].ycc, hp + p_ycc[c], size_t(Tcc) * N * 4, cudaMemcpyHostToDevice,
-                              C->s_aux));
-    }
-    SP_CUDA(cudaEventRecord(C->ev_ycc, C->s_aux));
-    SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_ycc, 0));
-  }
 
   // ---- finalize: reduce slices + CC partials + gates + cast ----
+  // Small CC partials are read by finalize_kernel straight from pinned host
+  // memory (unified addressing, no copy launch on the critical path); large
+  // ones (prompt blocks) are copied on the aux stream first.
+  constexpr size_t kZeroCopyYcc = size_t(256) << 10;
   FinalArgs fa{};
   fa.T = int(T);
   fa.N = int(N);
@@ -1092,13 +1161,30 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     fa.entry_row = fa.entry_call + total_rows;
     fa.entry_gate = reinterpret_cast<const float*>(fa.entry_row + total_rows);
   }
+  bool ycc_copy = false;
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int64_t Tcc = calls[c].tokens - calls[c].n_g;
-    fa.c[c] = FinalCall{ws[c].part, ws[c].S, (L->d.b1 > 0 && Tcc > 0) ? ws[c].ycc : nullptr, int(Tcc),
-                        int(calls[c].tokens)};
+    const bool has_cc = L->d.b1 > 0 && Tcc > 0;
+    const bool zc = size_t(Tcc) * N * 4 <= kZeroCopyYcc;
+    ycc_copy |= has_cc && !zc;
+    const float* ycc = !has_cc ? nullptr : zc ? reinterpret_cast<const float*>(hp + p_ycc[c]) : ws[c].ycc;
+    fa.c[c] = FinalCall{ws[c].part, ws[c].S, ycc, int(Tcc), int(calls[c].tokens)};
   }
-  {
+  // The tail runs on whichever thread finishes last: this one (GPU work all
+  // enqueued) or the CC coordinator (CC block done) -- so finalize is enqueued
+  // the moment both are ready, without a thread wake-up in between.
+  auto tail = [=]() -> int {
+    if (ycc_copy) {
+      for (int c = 0; c < n_calls; ++c) {
+        const int64_t Tcc = calls[c].tokens - calls[c].n_g;
+        if (fa.c[c].y_cc != ws[c].ycc) continue;
+        SP_CUDA(cudaMemcpyAsync(ws[c].ycc, hp + p_ycc[c], size_t(Tcc) * N * 4, cudaMemcpyHostToDevice,
+                                C->s_aux));
+      }
+      SP_CUDA(cudaEventRecord(C->ev_ycc, C->s_aux));
+      SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_ycc, 0));
+    }
     GpuSpan span(C, C->s_comp, 2, SP_TRACE_MERGE, 0.0);
     if (N % 4 == 0 && reinterpret_cast<uintptr_t>(fa.out) % 16 == 0) {
       dim3 grid(unsigned((N + 127) / 128), unsigned(T));
@@ -1110,14 +1196,22 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     SP_CUDA(cudaGetLastError());
     span.end();
     ++C->launches;
+    if (host_io)
+      SP_CUDA(cudaMemcpyAsync(hp + p_y, dws + o_ydev, size_t(T) * N * yel, cudaMemcpyDeviceToHost, C->s_comp));
+    else
+      SP_CUDA(cudaEventRecord(C->ev_done, C->s_comp));
+    return SP_OK;
+  };
+  if (need_cc && cc_async) {
+    SP_TRY(cc_join_with_tail(C, tail));
+  } else {
+    if (need_cc) SP_TRY(cc_work());
+    SP_TRY(tail());
   }
   if (host_io) {
-    SP_CUDA(cudaMemcpyAsync(hp + p_y, dws + o_ydev, size_t(T) * N * yel, cudaMemcpyDeviceToHost,
-                            C->s_comp));
     SP_CUDA(cudaStreamSynchronize(C->s_comp));
     memcpy(y, hp + p_y, size_t(T) * N * yel);
   } else {
-    SP_CUDA(cudaEventRecord(C->ev_done, C->s_comp));
     SP_CUDA(cudaStreamWaitEvent(user, C->ev_done, 0));
   }
   if (C->trace.on) ++C->trace.call;
@@ -1343,7 +1437,12 @@ int sp_layer_create(const sp_layer_desc* desc, const void* w1t, const void* w3t,
   int st = pack_layer(L.get(), w1t, d.gated ? w3t : nullptr, w2);
   if (st != SP_OK) {
     if (L->gg) cudaFree(L->gg);
-    if (L->host) L->host_only ? free(L->host) : (void)cudaFreeHost(L->host);
+    if (L->host && L->host_map_bytes) {
+    cudaHostUnregister(L->host);
+    munmap(L->host, L->host_map_bytes);
+  } else if (L->host) {
+    L->host_only ? free(L->host) : (void)cudaFreeHost(L->host);
+  }
     return st;
   }
   if (C->host_only) {
@@ -1368,7 +1467,12 @@ int sp_layer_destroy(sp_layer_t L) {
     cudaStreamSynchronize(C->s_copy);
   }
   if (L->gg) cudaFree(L->gg);
-  if (L->host) L->host_only ? free(L->host) : (void)cudaFreeHost(L->host);
+  if (L->host && L->host_map_bytes) {
+    cudaHostUnregister(L->host);
+    munmap(L->host, L->host_map_bytes);
+  } else if (L->host) {
+    L->host_only ? free(L->host) : (void)cudaFreeHost(L->host);
+  }
   delete L;
   return SP_OK;
 }

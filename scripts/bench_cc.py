@@ -25,13 +25,14 @@ def main():
         big.sum()
     print(f"numpy sum read: {3 * big.nbytes / (time.perf_counter() - t) / 1e9:.1f} GB/s (1 thread)")
     flush = np.zeros(64 << 20)
-    for H in (2048, 6144):
+    quick = "--quick" in sys.argv
+    for H in ((6144,) if quick else (2048, 6144)):
         w1t = rng.standard_normal((H, M), dtype=np.float32)
         w2 = rng.standard_normal((H, N), dtype=np.float32)
         lay = NativeLayer(w1t, w2, H, H, "silu", w1t, dtype="bf16")
         nbytes = lay.placed_bytes()["cc"]
         x = rng.standard_normal((1, M))
-        for th in [1, 4, 8, 12, 15, 16, os.cpu_count()]:
+        for th in ([8, os.cpu_count()] if quick else [1, 4, 8, 12, 15, 16, os.cpu_count()]):
             ts = []
             for r in range(6):
                 flush += 1
