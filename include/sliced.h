@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 1
+#define SP_ABI_VERSION 2
 
 typedef enum sp_status {
   SP_OK = 0,
@@ -161,6 +161,11 @@ typedef struct sp_trace_record {
   int32_t call;   /* forward sequence number since sp_trace_enable        */
   double start_s, end_s;
   double bytes;   /* weight bytes moved or touched                        */
+  double dev_s;   /* ffn_block launches: device-side duration, first CTA
+                   * start to last CTA end (%globaltimer); 0 otherwise.
+                   * start_s/end_s (CUDA events) also hold the launch's
+                   * front-end latency, which grows by ~23 us while the
+                   * copy engine saturates the host link.                 */
 } sp_trace_record;
 /* on != 0 clears the trace and starts recording (events on the library's own
  * streams, host clock for CC); sp_trace_fetch synchronises the device. */

@@ -60,6 +60,7 @@ class TraceRecord(C.Structure):
         ("start_s", C.c_double),
         ("end_s", C.c_double),
         ("bytes", C.c_double),
+        ("dev_s", C.c_double),
     ]
 
 
@@ -170,7 +171,8 @@ def trace_fetch() -> list[dict]:
     check(lib().sp_trace_fetch(buf, C.byref(n)))
     return [
         {"gemm_index": r.index, "stream": STREAM_NAMES[r.stream], "start_s": r.start_s,
-         "end_s": r.end_s, "kind": TRACE_KINDS[r.kind], "call": r.call, "bytes": r.bytes}
+         "end_s": r.end_s, "kind": TRACE_KINDS[r.kind], "call": r.call, "bytes": r.bytes,
+         "dev_s": r.dev_s}
         for r in buf[: n.value]
     ]
 

@@ -182,6 +182,8 @@ struct FfnArgs {
   float* part;
   int64_t slice0, slice_stride;
   unsigned long long* stamps;  // debug timing: [grid][8] %globaltimer stamps, or null
+  unsigned long long* kspan0;  // trace: atomicMin of every CTA's start (%globaltimer ns), or null
+  unsigned long long* kspan1;  // trace: atomicMax of every CTA's end
   int cta0, ncta;              // this block's CTAs inside a grouped launch
 };
 
@@ -229,6 +231,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   SP_STAMP(0);
+  if (p.kspan0 && threadIdx.x == 0) atomicMin(p.kspan0, global_ns());
   const int64_t r_begin = (int64_t)p.rows * cta / ncta;
   const int64_t r_end = (int64_t)p.rows * (cta + 1) / ncta;
   const int n_local = int(r_end - r_begin);
@@ -481,6 +484,10 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
     }
   }
   SP_STAMP(6);
+  if (p.kspan1) {
+    consumers_sync();
+    if (threadIdx.x == 0) atomicMax(p.kspan1, global_ns());
+  }
 }
 
 // ---- finalize: slice reduction + CC partial + MoE gates + cast, one launch -------------

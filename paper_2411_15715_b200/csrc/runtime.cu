@@ -113,6 +113,7 @@ constexpr int kRingSlots = 3;
 // host clock (launch / CC spans), both relative to one synchronised origin.
 struct Span {
   cudaEvent_t a = nullptr, b = nullptr;  // GPU span
+  int kslot = -1;                        // kernel-side span slot (ffn_block launches)
   double ha = 0, hb = 0;                 // host span (seconds since host_t0)
   int stream, kind, call;
   double bytes;
@@ -124,7 +125,12 @@ struct Trace {
   int call = 0;
   std::vector<Span> spans;
   std::vector<cudaEvent_t> pool;
+  // kernel-side spans: starts[kKSlots] (init ~0) | ends[kKSlots] (init 0), device
+  unsigned long long* kspan = nullptr;
+  int kspan_next = 0;
+  int kslot_cur = -1;  // slot of the GpuSpan being enqueued, picked up by ffn_args
 };
+constexpr int kKSlots = 16384;
 
 struct Context {
   int device = -1;
@@ -632,6 +638,10 @@ static FfnArgs ffn_args(Context* C, const sp_layer* L, const BlockView& b, const
            ((size_t(ldx) * esz_x) % 16 == 0) && (L->d.model_dim % vx == 0);
   a.part = w.part;
   a.stamps = C->stamps;
+  if (C->trace.kslot_cur >= 0) {
+    a.kspan0 = C->trace.kspan + C->trace.kslot_cur;
+    a.kspan1 = C->trace.kspan + kKSlots + C->trace.kslot_cur;
+  }
   a.slice0 = w.S;
   a.slice_stride = T_e * L->d.out_dim;
   return a;
@@ -700,10 +710,16 @@ struct GpuSpan {
     sp.bytes = bytes;
     sp.a = trace_event(C);
     sp.b = trace_event(C);
+    if (C->trace.kspan && (kind == SP_TRACE_GG || kind == SP_TRACE_CG || kind == SP_TRACE_CG_PRIME) &&
+        C->trace.kspan_next < kKSlots) {
+      sp.kslot = C->trace.kspan_next++;
+      C->trace.kslot_cur = sp.kslot;
+    }
     cudaEventRecord(sp.a, s);
   }
   void end() {
     if (!on) return;
+    C->trace.kslot_cur = -1;
     cudaEventRecord(sp.b, s);
     std::lock_guard<std::mutex> g(C->trace_mu);
     C->trace.spans.push_back(sp);
@@ -1109,6 +1125,11 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       // ends long before the last chunk kernel needs the stream.
       if (!items.empty()) SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_copied[items[0].slot], 0));
       GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, bytes);
+      if (C->trace.kslot_cur >= 0)
+        for (int i = 0; i < g.n; ++i) {
+          g.a[i].kspan0 = C->trace.kspan + C->trace.kslot_cur;
+          g.a[i].kspan1 = C->trace.kspan + kKSlots + C->trace.kslot_cur;
+        }
       SP_TRY(launch_group(C, calls[group[0]].layer, tt, g, cta, C->s_comp));
       span.end();
     }
@@ -1558,7 +1579,12 @@ int sp_trace_enable(int on) {
   tr.spans.clear();
   tr.call = 0;
   tr.on = on != 0;
+  tr.kspan_next = 0;
+  tr.kslot_cur = -1;
   if (tr.on) {
+    if (!tr.kspan) SP_CUDA(cudaMalloc(&tr.kspan, size_t(2) * kKSlots * sizeof(unsigned long long)));
+    SP_CUDA(cudaMemset(tr.kspan, 0xff, size_t(kKSlots) * sizeof(unsigned long long)));
+    SP_CUDA(cudaMemset(tr.kspan + kKSlots, 0, size_t(kKSlots) * sizeof(unsigned long long)));
     if (!tr.t0) SP_CUDA(cudaEventCreate(&tr.t0));
     SP_CUDA(cudaEventRecord(tr.t0, C->s_comp));
     SP_CUDA(cudaEventSynchronize(tr.t0));
@@ -1581,6 +1607,11 @@ int sp_trace_fetch(sp_trace_record* out, int* n) {
   SP_CUDA(cudaDeviceSynchronize());
   const int k = std::min(*n, have);
   int counters[4] = {0, 0, 0, 0};
+  std::vector<unsigned long long> ks;
+  if (tr.kspan && tr.kspan_next > 0) {
+    ks.resize(size_t(2) * kKSlots);
+    SP_CUDA(cudaMemcpy(ks.data(), tr.kspan, ks.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  }
   for (int i = 0; i < k; ++i) {
     const Span& sp = tr.spans[i];
     sp_trace_record r{};
@@ -1589,6 +1620,10 @@ int sp_trace_fetch(sp_trace_record* out, int* n) {
     r.kind = sp.kind;
     r.call = sp.call;
     r.bytes = sp.bytes;
+    if (sp.kslot >= 0 && !ks.empty()) {
+      const unsigned long long k0 = ks[size_t(sp.kslot)], k1 = ks[size_t(kKSlots + sp.kslot)];
+      r.dev_s = k1 > k0 ? double(k1 - k0) * 1e-9 : 0.0;
+    }
     if (sp.a) {
       float ma = 0, mb = 0;
       SP_CUDA(cudaEventElapsedTime(&ma, tr.t0, sp.a));

@@ -2,6 +2,8 @@
 Two GG-only experts (4096 x 7168 rows each, bf16 SwiGLU) in one forward,
 CUDA-event span of the grouped launch: alone, with background H2D copies,
 with a background host CC block, with both; L2 flushed between reps."""
+import ctypes as C
+import os
 import sys
 import threading
 import time
@@ -25,8 +27,22 @@ x = torch.randn(1, M, device="cuda").to(torch.bfloat16)
 nbytes = sum(l.placed_bytes()["gg"] for l in lays)
 
 
+lib = nat.lib()
+lib.sp_debug_stamps.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+STAMPS = os.environ.get("SP_KSTAMPS") == "1"
+
+
+def kernel_span():
+    """device-side duration of the last ffn_block launch: first CTA start to last CTA end"""
+    buf = (C.c_ulonglong * (4096 * 8))()
+    nat.check(lib.sp_debug_stamps(buf, 4096 * 8))
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 8)
+    a = a[a[:, 0] > 0]
+    return (a[:, 6].max() - a[:, 0].min()) * 1e-9
+
+
 def sample(reps=20):
-    ts = []
+    ts, ks = [], []
     for r in range(reps):
         scratch.add_(1.0)
         torch.cuda.synchronize()
@@ -37,7 +53,11 @@ def sample(reps=20):
         nat.trace_enable(False)
         if r >= 3:
             ts.append(sp[0]["end_s"] - sp[0]["start_s"])
+            if STAMPS:
+                ks.append(kernel_span())
     t = float(np.median(ts))
+    if ks:
+        print(f"    (in-kernel span {np.median(ks) * 1e6:.1f} us)", flush=True)
     return t, nbytes / t / 1e9
 
 
@@ -46,7 +66,12 @@ def busy_gpu():
     return None
 
 
-print(f"alone:            {sample()[0]*1e6:7.1f} us  {sample()[1]:7.0f} GB/s", flush=True)
+t, bw = sample()
+print(f"alone:            {t*1e6:7.1f} us  {bw:7.0f} GB/s", flush=True)
+for mb in (8, 512):
+    with BackgroundCopy(torch, nbytes=mb << 20):
+        t, bw = sample()
+        print(f"+ H2D copies into {mb} MB: {t*1e6:7.1f} us  {bw:7.0f} GB/s", flush=True)
 with BackgroundCopy(torch):
     t, bw = sample()
     print(f"+ H2D copies:     {t*1e6:7.1f} us  {bw:7.0f} GB/s", flush=True)

@@ -39,7 +39,7 @@ def test_abi_version_and_struct_layouts():
     assert nat.lib().sp_abi_version() == int(re.search(r"SP_ABI_VERSION (\d+)", HEADER).group(1))
     assert C.sizeof(nat.LayerDesc) == 3 * 8 + 4 * 4 + 2 * 8
     assert C.sizeof(nat.Call) == 5 * 8
-    assert C.sizeof(nat.TraceRecord) == 4 * 4 + 3 * 8
+    assert C.sizeof(nat.TraceRecord) == 4 * 4 + 4 * 8
 
 
 def test_status_codes_map_to_reference_classes():
