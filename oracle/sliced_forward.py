@@ -89,6 +89,15 @@ def sliced_forward(x, w1, w2, act: str, cc: float, cg: float, w3=None) -> np.nda
     return out
 
 
+def dense_forward_bf16_hidden(x, w1, w2, act: str, w3=None) -> np.ndarray:
+    """dense_forward with the hidden activation rounded to bf16 before the down
+    projection: the arithmetic of a bf16 tile / tensor-core block (the GPU
+    tcgen05 GEMM pair and the host AMX CC kernel keep `a` in bf16)."""
+    x, w1, w2 = (np.asarray(a, dtype=float) for a in (x, w1, w2))
+    w3 = None if w3 is None else np.asarray(w3, dtype=float)
+    return bf16_round(_hidden(x, w1, w3, act)) @ w2
+
+
 def segment_forward(x, w1, w2, act: str, lo: int, hi: int, w3=None) -> np.ndarray:
     """One block's partial output (e.g. the CC slice alone)."""
     x, w1, w2 = (np.asarray(a, dtype=float) for a in (x, w1, w2))

@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_native"
 LIB = OUT_DIR / "libsliced.so"
-SOURCES = ["runtime.cu", "host_cc.cpp"]
+SOURCES = ["runtime.cu", "host_cc.cpp", "host_cc_amx.cpp"]
 HEADERS = ["kernels.cuh", "gemm_tc.cuh", "host_cc.h", "../../include/sliced.h"]
 
 NVCC_FLAGS = [

@@ -20,6 +20,8 @@ static int env_or(const char* name, int dflt) {
   return v && *v ? atoi(v) : dflt;
 }
 static const int g_cc_pf = env_or("SP_CC_PREFETCH", 0);
+static const int g_amx = env_or("SP_AMX", 1);
+static const int g_amx_min_t = env_or("SP_AMX_MIN_T", 4);
 
 // ---------------------------------------------------------------------------
 // thread pool: persistent workers, the caller participates as tid 0
@@ -258,6 +260,7 @@ void cc_forward(const CCProblem& p, ThreadPool& pool, int threads) {
     return;
   }
   const int wd = p.wdtype;
+  if (wd == 1 && g_amx && T >= g_amx_min_t && host_has_amx()) return cc_forward_amx(p, pool, threads);
   const size_t esz = wd == 1 ? 2 : 4;
   const int64_t k_up = round16(p.M);
   const int64_t n16 = round16(p.N);  // W2 rows are zero padded to ldn >= roundup(N, 64)
@@ -278,7 +281,11 @@ void cc_forward(const CCProblem& p, ThreadPool& pool, int threads) {
   const int64_t budget = (int64_t(8) << 20) / (slice * 4);  // partial slices within 8 MB
   int64_t nb = std::min<int64_t>(p.b1, std::max<int64_t>(n_thr, std::min<int64_t>(budget, 8 * n_thr)));
   nb = std::max<int64_t>(1, nb);
-  std::vector<float> ybufs(size_t(nb) * slice);
+  // persistent across calls (no page faults on fresh mmap'd memory every call)
+  // (a thread_local is per thread: the workers below must use this pointer)
+  static thread_local std::vector<float> tl_ybufs;
+  tl_ybufs.resize(std::max(tl_ybufs.size(), size_t(nb) * slice));
+  float* const ybufs = tl_ybufs.data();
   std::atomic<int64_t> cursor{0};
 
   auto rows_pass = [&](int, int) {
@@ -288,7 +295,7 @@ void cc_forward(const CCProblem& p, ThreadPool& pool, int threads) {
       const int64_t blk = cursor.fetch_add(1, std::memory_order_relaxed);
       if (blk >= nb) break;
       const int64_t h0 = p.b1 * blk / nb, h1 = p.b1 * (blk + 1) / nb;
-      float* ybuf = ybufs.data() + size_t(blk) * slice;
+      float* ybuf = ybufs + size_t(blk) * slice;
       std::fill(ybuf, ybuf + slice, 0.f);
       int pend = 0;
       for (int64_t h = h0; h < h1; ++h) {
@@ -321,7 +328,7 @@ void cc_forward(const CCProblem& p, ThreadPool& pool, int threads) {
     for (int64_t t = 0; t < T; ++t) {
       std::fill(acc.begin(), acc.end(), 0.f);
       for (int64_t i = 0; i < nb; ++i) {  // block order: deterministic
-        const float* src = ybufs.data() + size_t(i) * slice + t * n16;
+        const float* src = ybufs + size_t(i) * slice + t * n16;
         for (int64_t col = c0; col < c1; ++col) acc[size_t(col - c0)] += src[col];
       }
       std::copy(acc.begin(), acc.end(), p.y + t * p.N + c0);

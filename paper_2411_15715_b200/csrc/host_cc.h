@@ -64,5 +64,10 @@ struct CCProblem {
 
 void cc_forward(const CCProblem& p, ThreadPool& pool, int threads);
 bool host_has_avx512();
+// AMX tile path for bf16 weights and prompt-size token counts (host_cc_amx.cpp);
+// cc_forward dispatches to it when T >= SP_AMX_MIN_T (default 4) and the host
+// has AMX-BF16 (SP_AMX=0 disables it).
+bool host_has_amx();
+void cc_forward_amx(const CCProblem& p, ThreadPool& pool, int threads);
 
 }  // namespace sp
