@@ -109,9 +109,11 @@ def test_cc_host_kernel_matches_oracle(host_ctx, dtype, gated, act):
         q = orc.bf16_round if dtype == "bf16" else (lambda a: a)
         ref = orc.dense_forward(q(x), q(w1), q(w2), act, q(w3) if gated else None)
         if dtype == "bf16" and T >= 4 and host_has_amx():
-            # AMX tile path: the hidden activation is rounded to bf16 (as on the GPU tensor cores)
+            # AMX tile path: the hidden activation is rounded to bf16 (as on the GPU tensor
+            # cores); fp32 vs fp64 pre-activations can land on opposite sides of a bf16
+            # rounding boundary, a one-ulp (2^-8) flip of single hidden units
             ref_h = orc.dense_forward_bf16_hidden(q(x), q(w1), q(w2), act, q(w3) if gated else None)
-            assert orc.max_rel_error(got, ref_h) <= 1e-4
+            assert orc.max_rel_error(got, ref_h) <= 5e-4
             assert orc.max_rel_error(got, ref) <= 5e-3
             continue
         assert orc.max_rel_error(got, ref) <= 1e-5
