@@ -548,6 +548,23 @@ def run_prefill_decode(args):
     clk.stop()
     ng_used = {t: n for t, n in sorted(ng_cache.items())}
     t_e_prompt = sorted({len(c.token_ids) for c in prompt_plans[0]})
+    if args.trace_out:
+        nat.trace_enable(True)
+        prefill()
+        torch.cuda.synchronize()
+        Path(args.trace_out).write_text(json.dumps([s for s in nat.trace_fetch() if s["call"] < 4], indent=0))
+        nat.trace_enable(False)
+        # the same through the host-I/O public API (x / y in host memory)
+        nat.trace_enable(True)
+        t0 = time.perf_counter()
+        for l in range(min(4, args.layers)):
+            forward_calls(prompt_plans[l % D], xp_host)
+        torch.cuda.synchronize()
+        host_wall = (time.perf_counter() - t0) / min(4, args.layers)
+        Path(args.trace_out.replace(".json", "_hostio.json")).write_text(
+            json.dumps([s for s in nat.trace_fetch() if s["call"] < 4], indent=0))
+        nat.trace_enable(False)
+        print(f"host-I/O prefill layer wall: {host_wall * 1e3:.1f} ms", flush=True)
     # host-I/O prefill through the public API
     t_e2e = timed(lambda: [forward_calls(prompt_plans[l % D], xp_host) for l in range(args.layers)])
     line = {

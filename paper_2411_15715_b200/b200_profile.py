@@ -276,7 +276,7 @@ def measure(phase: str = "decode", quick: bool = False, load: str = "concurrent"
     nat.init(0)
     gpu_tokens, cpu_tokens = (1, 1) if phase == "decode" else (128, 32)
     widths = [256, 1024, 2048, 4096, 7168, 10240, 14336]
-    cpu_widths = [128, 256, 512, 1024, 2048, 4096] if phase == "decode" else [64, 128, 256, 512]
+    cpu_widths = [128, 256, 512, 1024, 2048, 4096] if phase == "decode" else [256, 1024, 2048, 4096]
     if quick:
         widths, cpu_widths = [1024, 4096, 14336], cpu_widths[:3]
     if load == "concurrent":
