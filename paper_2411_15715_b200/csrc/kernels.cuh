@@ -493,9 +493,13 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
 // ---- finalize: slice reduction + CC partial + MoE gates + cast, one launch -------------
 //   y[t, n] = sum over entries (c, i, gate) of token t (host-built CSR, in call order)
 //             of gate * (sum_s part_c[s, i, n] + y_cc_c[i, n])
-// Block = (128 output columns as 32 float4 lanes) x 8 slice groups, one output
-// token per blockIdx.y.  Every sum runs in a fixed order -> deterministic.
+// Block = (32 output columns as 8 float4 lanes) x 32 slice groups, one output
+// token per blockIdx.y: N/32 blocks per token, so a decode step's few hundred
+// partial slices are read by ~128 CTAs instead of 32.  Every sum runs in a
+// fixed order -> deterministic.
 constexpr int kMaxCalls = 32;
+constexpr int kFinLanes = 8;    // float4 column lanes per block
+constexpr int kFinGroups = 32;  // slice groups per block
 struct FinalCall {
   const float* part;     // [S][T_e][N] partial slices
   int S;
@@ -515,10 +519,10 @@ struct FinalArgs {
   int odtype;
 };
 
-__global__ void __launch_bounds__(256) finalize_kernel(FinalArgs p) {
-  __shared__ float4 red[8][32];
-  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
-  const int n = (blockIdx.x * 32 + lane) * 4;
+__global__ void __launch_bounds__(kFinLanes * kFinGroups) finalize_kernel(FinalArgs p) {
+  __shared__ float4 red[kFinGroups][kFinLanes];
+  const int lane = threadIdx.x % kFinLanes, grp = threadIdx.x / kFinLanes;
+  const int n = (blockIdx.x * kFinLanes + lane) * 4;
   const int t = blockIdx.y;
   const bool live = n < p.N;  // N % 4 == 0 on this path
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -530,13 +534,13 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalArgs p) {
       const int64_t stride = int64_t(fc.T_e) * p.N;
       const float* base = fc.part + int64_t(i) * p.N + n;
       int s = grp;
-      for (; s + 8 < fc.S; s += 16) {
+      for (; s + kFinGroups < fc.S; s += 2 * kFinGroups) {
         const float4 a = __ldcg(reinterpret_cast<const float4*>(base + int64_t(s) * stride));
-        const float4 b = __ldcg(reinterpret_cast<const float4*>(base + int64_t(s + 8) * stride));
+        const float4 b = __ldcg(reinterpret_cast<const float4*>(base + int64_t(s + kFinGroups) * stride));
         v0.x += a.x; v0.y += a.y; v0.z += a.z; v0.w += a.w;
         v1.x += b.x; v1.y += b.y; v1.z += b.z; v1.w += b.w;
       }
-      for (; s < fc.S; s += 8) {
+      for (; s < fc.S; s += kFinGroups) {
         const float4 a = __ldcg(reinterpret_cast<const float4*>(base + int64_t(s) * stride));
         v0.x += a.x; v0.y += a.y; v0.z += a.z; v0.w += a.w;
       }
@@ -545,8 +549,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalArgs p) {
     __syncthreads();
     if (grp == 0 && live) {
       float4 tot = red[0][lane];
-#pragma unroll
-      for (int g = 1; g < 8; ++g) {
+#pragma unroll 8
+      for (int g = 1; g < kFinGroups; ++g) {
         const float4 r = red[g][lane];
         tot.x += r.x; tot.y += r.y; tot.z += r.z; tot.w += r.w;
       }

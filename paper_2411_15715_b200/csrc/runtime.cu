@@ -1208,8 +1208,8 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     }
     GpuSpan span(C, C->s_comp, 2, SP_TRACE_MERGE, 0.0);
     if (N % 4 == 0 && reinterpret_cast<uintptr_t>(fa.out) % 16 == 0) {
-      dim3 grid(unsigned((N + 127) / 128), unsigned(T));
-      finalize_kernel<<<grid, 256, 0, C->s_comp>>>(fa);
+      dim3 grid(unsigned((N + 4 * kFinLanes - 1) / (4 * kFinLanes)), unsigned(T));
+      finalize_kernel<<<grid, kFinLanes * kFinGroups, 0, C->s_comp>>>(fa);
     } else {
       dim3 grid(unsigned(std::min<int64_t>((N + 255) / 256, 64)), unsigned(T));
       finalize_scalar_kernel<<<grid, 256, 0, C->s_comp>>>(fa);
