@@ -111,6 +111,19 @@ def load_profile(path):
     return costs.profile_from_dict(FALLBACK_DECODE), "fallback (b200_profile.FALLBACK_DECODE)"
 
 
+def decode_profile_for(path, t_expert: int) -> str:
+    """The decode profile measured closest below the per-expert token count
+    (b200_decode_t<T>.json from ``b200_profile --tokens T``; T = 1 is the
+    default file): the cost model is linear in T, the kernels are not."""
+    p = Path(path)
+    best = p
+    for t in (2, 4, 8):
+        q = p.with_name(f"{p.stem}_t{t}{p.suffix}")
+        if t <= t_expert and q.exists():
+            best = q
+    return str(best)
+
+
 def expected_active(experts: int, top_k: int, batch: int) -> float:
     """Expected distinct experts a batch of `batch` tokens touches with uniform top-k routing."""
     return experts * (1.0 - (1.0 - top_k / experts) ** batch)
@@ -127,12 +140,12 @@ def plan_rates(args, tokens_per_step):
 
     import paper_2411_15715_b200 as sp
 
-    profile, source = load_profile(args.profile)
     hidden = getattr(args, "shard_hidden", args.hidden_dim)
     e_act = min(expected_active(args.experts, args.top_k, tokens_per_step), args.experts) if args.experts > 1 \
         else 1.0
     n_gemms = max(args.top_k, round(e_act)) * 3
     t_expert = max(1, math.ceil(tokens_per_step * args.top_k / max(e_act, 1.0)))
+    profile, source = load_profile(decode_profile_for(args.profile, t_expert))
     layer = sp.LayerSpec(args.model_dim, hidden, n_gemms=n_gemms, precision=sp.Precision.FP16)
     budget = args.budget_frac * layer.layer_bytes
     if args.config == "cfg1":

@@ -204,7 +204,7 @@ def c2g_samples(torch, chunk_rows=(32, 64, 128, 320, 640, 1280), reps=3, model_d
 
 
 def insitu_samples(torch, cc_rates=(0.1, 0.2, 0.3, 0.4), r_gg=0.5, model_dim=4096, hidden=14336,
-                   experts=2, reps=6, seed=11):
+                   experts=2, reps=6, seed=11, tokens=1):
     """CPU GEMM and chunk-copy samples taken from real sliced decode steps.
 
     For each CC rate, `experts` SwiGLU experts are placed with rates
@@ -218,7 +218,7 @@ def insitu_samples(torch, cc_rates=(0.1, 0.2, 0.3, 0.4), r_gg=0.5, model_dim=409
     g = torch.Generator(device="cuda").manual_seed(seed)
     mk = lambda *s: (torch.randn(*s, device="cuda", generator=g) / 64).to(torch.bfloat16).cpu()  # noqa: E731
     weights = [(mk(hidden, model_dim), mk(hidden, model_dim), mk(hidden, model_dim)) for _ in range(experts)]
-    x = torch.randn(1, model_dim, device="cuda").to(torch.bfloat16)
+    x = torch.randn(tokens, model_dim, device="cuda").to(torch.bfloat16)
     out = []
     for cc in cc_rates:
         b1 = int(np.floor(cc * hidden))
@@ -236,7 +236,8 @@ def insitu_samples(torch, cc_rates=(0.1, 0.2, 0.3, 0.4), r_gg=0.5, model_dim=409
             for s_ in spans:
                 dt = s_["end_s"] - s_["start_s"]
                 if s_["kind"] == "cc":
-                    out.append(ProfileSample(OpClass.CPU_GEMM, float(model_dim) * b1, dt / 3.0, Precision.FP16))
+                    out.append(ProfileSample(OpClass.CPU_GEMM, float(tokens) * model_dim * b1, dt / 3.0,
+                                             Precision.FP16))
                 elif s_["kind"] == "copy":
                     out.append(ProfileSample(OpClass.C2G, float(s_["bytes"]), dt))
         for l in lays:
@@ -266,15 +267,19 @@ def launch_samples(torch, reps=20):
     return out
 
 
-def measure(phase: str = "decode", quick: bool = False, load: str = "concurrent") -> list[ProfileSample]:
-    """decode: T = 1 everywhere.  prompt: the GPU GEMM at T = 128 tokens (an
-    expert's share of a 512-token top-2 prompt, tensor-core path) and the host
-    GEMM at T = 32 -- one profile per phase, because t_G = alpha + T*M*H*beta
-    (pipeline.py:163) is linear in T while a GEMV/GEMM is not."""
+def measure(phase: str = "decode", quick: bool = False, load: str = "concurrent",
+            tokens: int = 1) -> list[ProfileSample]:
+    """decode: ``tokens`` per expert everywhere (1 = single-token decode; 2..8
+    for batched decode, where each active expert sees a few tokens).  prompt:
+    the GPU GEMM at T = 128 tokens (an expert's share of a 512-token top-2
+    prompt, tensor-core path) and the host GEMM at T = 32.  One profile per
+    regime, because t_G = alpha + T*M*H*beta (pipeline.py:163) is linear in T
+    while a weight-streaming GEMV (and the host CC block) costs nearly the same
+    for 1 or 4 tokens."""
     import torch
 
     nat.init(0)
-    gpu_tokens, cpu_tokens = (1, 1) if phase == "decode" else (128, 32)
+    gpu_tokens, cpu_tokens = (tokens, tokens) if phase == "decode" else (128, 32)
     widths = [256, 1024, 2048, 4096, 7168, 10240, 14336]
     cpu_widths = [128, 256, 512, 1024, 2048, 4096] if phase == "decode" else [256, 1024, 2048, 4096]
     if quick:
@@ -286,7 +291,7 @@ def measure(phase: str = "decode", quick: bool = False, load: str = "concurrent"
         with BackgroundCopy(torch):
             samples = gpu_gemm_samples(torch, gpu_tokens, widths, reps=3 if quick else 5)
         if phase == "decode":
-            samples += insitu_samples(torch, reps=3 if quick else 6)
+            samples += insitu_samples(torch, reps=3 if quick else 6, tokens=tokens)
         else:
             with BackgroundCopy(torch):
                 samples += cpu_gemm_samples(cpu_tokens, cpu_widths, reps=2 if quick else 4)
@@ -304,16 +309,19 @@ def main(argv=None) -> None:
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--out", default="profiles")
     ap.add_argument("--phase", default="decode", choices=["decode", "prompt"])
+    ap.add_argument("--tokens", type=int, default=1,
+                    help="decode: tokens per expert (batched decode); writes b200_decode_t<T>.json for T > 1")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--load", default="concurrent", choices=["concurrent", "isolated"],
                     help="sample the host-side rates under each other's host-DRAM load (default) or alone")
     args = ap.parse_args(argv)
     out = Path(args.out)
     out.mkdir(parents=True, exist_ok=True)
-    samples = measure(args.phase, args.quick, args.load)
-    write_samples_csv(samples, out / f"b200_samples_{args.phase}.csv")
-    prof, warns = fit_profile(samples, f"b200-{args.phase}" + ("" if args.load == "concurrent" else "-isolated"))
-    (out / f"b200_{args.phase}.json").write_bytes(save_profile(prof))
+    samples = measure(args.phase, args.quick, args.load, args.tokens)
+    tag = args.phase if args.phase == "prompt" or args.tokens == 1 else f"{args.phase}_t{args.tokens}"
+    write_samples_csv(samples, out / f"b200_samples_{tag}.csv")
+    prof, warns = fit_profile(samples, f"b200-{tag}" + ("" if args.load == "concurrent" else "-isolated"))
+    (out / f"b200_{tag}.json").write_bytes(save_profile(prof))
     g = prof.gemm[Precision.FP16]
     summary = {
         "gpu_gemm_effective_GBps": 2.0 / g.gpu.beta / 1e9 if g.gpu.beta else None,

@@ -99,6 +99,35 @@ float span_behind_copy(cudaStream_t s, cudaStream_t c, void* d, void* h, int* ou
   return v[v.size() / 2];
 }
 
+// A ~60 us kernel: is the extra latency under a busy link at the start or the end of the span?
+__global__ void spin(long long cycles, int* out) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < cycles) {
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) *out = 2;
+}
+
+float span_spin(cudaStream_t s, int* out, long long cycles, cudaStream_t c, void* d, void* h, int mode, int reps) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  std::vector<float> v;
+  for (int r = 0; r < reps; ++r) {
+    cudaDeviceSynchronize();
+    if (mode == 1) cudaMemcpyAsync(d, h, size_t(64) << 20, cudaMemcpyHostToDevice, c);  // link busy first
+    cudaEventRecord(a, s);
+    spin<<<148, 128, 0, s>>>(cycles, out);
+    cudaEventRecord(b, s);
+    if (mode == 2) cudaMemcpyAsync(d, h, size_t(64) << 20, cudaMemcpyHostToDevice, c);  // link busy after launch
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    v.push_back(ms * 1000.f);
+  }
+  std::sort(v.begin(), v.end());
+  return v[v.size() / 2];
+}
+
 int main() {
   cudaStream_t s, c;
   cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
@@ -124,5 +153,9 @@ int main() {
   for (int i = 0; i < 40; ++i) cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, c2);
   printf("queued behind a copy event, link busy: 2 KB %.1f us\n", span_behind_copy<2048>(s, c, (char*)d + (size_t(128) << 20), h, out, 21));
   cudaStreamSynchronize(c2);
+  const long long cyc = 60LL * 1965;  // ~60 us at 1965 MHz
+  printf("60us spin kernel: idle link %.1f us | copy started before %.1f us | copy started after launch %.1f us\n",
+         span_spin(s, out, cyc, c, d, h, 0, 21), span_spin(s, out, cyc, c, d, h, 1, 21),
+         span_spin(s, out, cyc, c, d, h, 2, 21));
   return 0;
 }
