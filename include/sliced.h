@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 2
+#define SP_ABI_VERSION 3
 
 typedef enum sp_status {
   SP_OK = 0,
@@ -110,6 +110,27 @@ int sp_layer_destroy(sp_layer_t layer);
 int sp_layer_bytes(sp_layer_t layer, size_t* gg, size_t* cg, size_t* cc);
 /* Block widths (cc, cg, gg) == SlicedWeights.block_widths (slicing_kernel.py:50-54). */
 int sp_layer_widths(sp_layer_t layer, int64_t widths[3]);
+
+/* ---- sliced weight store ---------------- */
+/* A placed layer's two images: the GG block exactly as it sits in HBM
+ * (W1t | W3t | W2 rows [b2, H), rows zero padded to 64 elements) and the
+ * pinned host region (CC then CG chunks of chunk_rows hidden units, each
+ * W1t | W3t | W2, 4 KB aligned).  Saving the images and creating a layer from
+ * them skips the repack: a straight read into pinned memory plus one HBM
+ * upload.  The desc must carry the chunk_rows the images were packed with
+ * (sp_layer_image_sizes reports it). */
+int sp_layer_image_sizes(sp_layer_t layer, size_t* gg_bytes, size_t* host_bytes, int32_t* chunk_rows);
+/* Copy the images out (either destination may be NULL). */
+int sp_layer_export(sp_layer_t layer, void* gg_dst, void* host_dst);
+int sp_layer_create_from_images(const sp_layer_desc* desc, const void* gg_img, size_t gg_bytes,
+                                const void* host_img, size_t host_bytes, sp_layer_t* out);
+/* Same, reading the images from a file at the given offsets (the host image
+ * lands directly in the layer's pinned region). */
+int sp_layer_load_file(const sp_layer_desc* desc, const char* path, uint64_t gg_offset, size_t gg_bytes,
+                       uint64_t host_offset, size_t host_bytes, sp_layer_t* out);
+/* Re-slice a placed layer to new boundaries b1 <= b2 (the rates changed,
+ * PAPER.md:103): rows are gathered back (GG rows from HBM) and re-placed. */
+int sp_layer_reslice(sp_layer_t layer, int64_t b1, int64_t b2, sp_layer_t* out);
 
 /* ---- forward (mlp_forward_sliced, slicing_kernel.py:97-124) ------------ */
 /* y[t, :] = sum over calls c, rows i with ids_c[i] == t of

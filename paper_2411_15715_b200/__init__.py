@@ -87,5 +87,6 @@ from .sliced import (
     mlp_forward_sliced,
     slice_weights,
 )
+from .store import load_mixtral_moe, load_safetensors, load_store, save_safetensors, save_store
 
 __version__ = "0.1.0"

@@ -66,6 +66,14 @@ class TraceRecord(C.Structure):
 
 SIGNATURES = {
     "sp_abi_version": (C.c_int, []),
+    "sp_layer_image_sizes": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                                       C.POINTER(C.c_int32)]),
+    "sp_layer_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sp_layer_create_from_images": (C.c_int, [C.POINTER(LayerDesc), C.c_void_p, C.c_size_t, C.c_void_p,
+                                              C.c_size_t, C.POINTER(C.c_void_p)]),
+    "sp_layer_load_file": (C.c_int, [C.POINTER(LayerDesc), C.c_char_p, C.c_uint64, C.c_size_t, C.c_uint64,
+                                     C.c_size_t, C.POINTER(C.c_void_p)]),
+    "sp_layer_reslice": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_void_p)]),
     "sp_last_error": (C.c_char_p, []),
     "sp_init": (C.c_int, [C.c_int, C.c_int]),
     "sp_shutdown": (C.c_int, []),

@@ -13,7 +13,9 @@
 #include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
+#include <fcntl.h>
 #include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
@@ -233,16 +235,15 @@ static void copy_rows(char* dst, int64_t ld, const char* src, int64_t cols, int6
 static int env_int(const char* name, int dflt);
 // SP_HUGEPAGES=1: CC/CG host region on 2 MB transparent huge pages (mmap + cudaHostRegister)
 static const bool g_hugepages = env_int("SP_HUGEPAGES", 0) != 0;
+// default CG/CC chunk size (MB) when the layer does not set chunk_rows
+static const int g_chunk_mb = std::max(1, env_int("SP_CHUNK_MB", 8));
 
-static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void* w2) {
+// Layout + allocation of a layer's GG block (HBM) and host region (pinned
+// CC then CG chunks); contents zeroed.  `fill_rows` / an image copy fill them.
+static int place_layer(sp_layer* L) {
   const sp_layer_desc& d = L->d;
-  const int64_t M = d.model_dim, H = d.hidden_dim, N = d.out_dim;
   const size_t esz = L->esz;
-  const char* s1 = static_cast<const char*>(w1t);
-  const char* s3 = static_cast<const char*>(w3t);
-  const char* s2 = static_cast<const char*>(w2);
   const int G = d.gated ? 2 : 1;
-  (void)H;
 
   // ---- GG block -> HBM ----
   L->h_gg = d.hidden_dim - d.b2;
@@ -255,21 +256,13 @@ static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void*
     L->gg_bytes = up * G + size_t(L->h_gg) * L->ldn * esz;
     SP_CUDA(cudaMalloc(&L->gg, L->gg_bytes));
     SP_CUDA(cudaMemset(L->gg, 0, L->gg_bytes));
-    char* g = static_cast<char*>(L->gg);
-    SP_CUDA(cudaMemcpy2D(g, L->ldm * esz, s1 + size_t(d.b2) * M * esz, M * esz, M * esz, L->h_gg,
-                         cudaMemcpyHostToDevice));
-    if (G == 2)
-      SP_CUDA(cudaMemcpy2D(g + L->gg_w3_off, L->ldm * esz, s3 + size_t(d.b2) * M * esz, M * esz,
-                           M * esz, L->h_gg, cudaMemcpyHostToDevice));
-    SP_CUDA(cudaMemcpy2D(g + L->gg_w2_off, L->ldn * esz, s2 + size_t(d.b2) * N * esz, N * esz,
-                         N * esz, L->h_gg, cudaMemcpyHostToDevice));
   }
 
   // ---- CC and CG blocks -> pinned host, chunk-interleaved ----
   int64_t cr = d.chunk_rows;
   if (cr <= 0) {
     const int64_t row_bytes = (G * L->ldm + L->ldn) * int64_t(esz);
-    cr = std::max<int64_t>(kPadElems, ((int64_t(8) << 20) / row_bytes) / kPadElems * kPadElems);
+    cr = std::max<int64_t>(kPadElems, ((int64_t(g_chunk_mb) << 20) / row_bytes) / kPadElems * kPadElems);
   }
   cr = round_up(cr, kPadElems);
   L->d.chunk_rows = int32_t(cr);
@@ -319,12 +312,66 @@ static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void*
       return fail(SP_ERR_NOMEM, "cudaHostAlloc(%zu) for the CC/CG blocks failed", off);
     }
     memset(L->host, 0, off);
-    char* h = static_cast<char*>(L->host);
-    for (const Chunk& c : L->chunks) {
-      char* base = h + c.off;
-      copy_rows(base, L->ldm, s1, M, c.r0, c.rc, esz);
-      if (G == 2) copy_rows(base + c.w3_off, L->ldm, s3, M, c.r0, c.rc, esz);
-      copy_rows(base + c.w2_off, L->ldn, s2, N, c.r0, c.rc, esz);
+  }
+  return SP_OK;
+}
+
+// Fill a placed layer from row-major sources: w1t / w3t [H, M], w2 [H, N].
+static int fill_rows(sp_layer* L, const void* w1t, const void* w3t, const void* w2) {
+  const sp_layer_desc& d = L->d;
+  const int64_t M = d.model_dim, N = d.out_dim;
+  const size_t esz = L->esz;
+  const char* s1 = static_cast<const char*>(w1t);
+  const char* s3 = static_cast<const char*>(w3t);
+  const char* s2 = static_cast<const char*>(w2);
+  if (L->h_gg > 0) {
+    char* g = static_cast<char*>(L->gg);
+    SP_CUDA(cudaMemcpy2D(g, L->ldm * esz, s1 + size_t(d.b2) * M * esz, M * esz, M * esz, L->h_gg,
+                         cudaMemcpyHostToDevice));
+    if (d.gated)
+      SP_CUDA(cudaMemcpy2D(g + L->gg_w3_off, L->ldm * esz, s3 + size_t(d.b2) * M * esz, M * esz,
+                           M * esz, L->h_gg, cudaMemcpyHostToDevice));
+    SP_CUDA(cudaMemcpy2D(g + L->gg_w2_off, L->ldn * esz, s2 + size_t(d.b2) * N * esz, N * esz,
+                         N * esz, L->h_gg, cudaMemcpyHostToDevice));
+  }
+  char* h = static_cast<char*>(L->host);
+  for (const Chunk& c : L->chunks) {
+    char* base = h + c.off;
+    copy_rows(base, L->ldm, s1, M, c.r0, c.rc, esz);
+    if (d.gated) copy_rows(base + c.w3_off, L->ldm, s3, M, c.r0, c.rc, esz);
+    copy_rows(base + c.w2_off, L->ldn, s2, N, c.r0, c.rc, esz);
+  }
+  return SP_OK;
+}
+
+static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void* w2) {
+  SP_TRY(place_layer(L));
+  return fill_rows(L, w1t, w3t, w2);
+}
+
+// Row-major [H, M] / [H, N] copies of a placed layer's weights (GG rows read
+// back from HBM): the input of a re-slice.
+static int gather_rows(const sp_layer* L, char* w1t, char* w3t, char* w2) {
+  const sp_layer_desc& d = L->d;
+  const int64_t M = d.model_dim, N = d.out_dim;
+  const size_t esz = L->esz;
+  if (L->h_gg > 0) {
+    const char* g = static_cast<const char*>(L->gg);
+    SP_CUDA(cudaMemcpy2D(w1t + size_t(d.b2) * M * esz, M * esz, g, L->ldm * esz, M * esz, L->h_gg,
+                         cudaMemcpyDeviceToHost));
+    if (d.gated)
+      SP_CUDA(cudaMemcpy2D(w3t + size_t(d.b2) * M * esz, M * esz, g + L->gg_w3_off, L->ldm * esz, M * esz,
+                           L->h_gg, cudaMemcpyDeviceToHost));
+    SP_CUDA(cudaMemcpy2D(w2 + size_t(d.b2) * N * esz, N * esz, g + L->gg_w2_off, L->ldn * esz, N * esz,
+                         L->h_gg, cudaMemcpyDeviceToHost));
+  }
+  const char* h = static_cast<const char*>(L->host);
+  for (const Chunk& c : L->chunks) {
+    const char* base = h + c.off;
+    for (int64_t r = 0; r < c.rc; ++r) {
+      memcpy(w1t + size_t(c.r0 + r) * M * esz, base + size_t(r) * L->ldm * esz, size_t(M) * esz);
+      if (d.gated) memcpy(w3t + size_t(c.r0 + r) * M * esz, base + c.w3_off + size_t(r) * L->ldm * esz, size_t(M) * esz);
+      memcpy(w2 + size_t(c.r0 + r) * N * esz, base + c.w2_off + size_t(r) * L->ldn * esz, size_t(N) * esz);
     }
   }
   return SP_OK;
@@ -1430,10 +1477,7 @@ int sp_shutdown(void) {
   return SP_OK;
 }
 
-int sp_layer_create(const sp_layer_desc* desc, const void* w1t, const void* w3t, const void* w2,
-                    sp_layer_t* out) {
-  if (!desc || !out || !w1t || !w2) return fail(SP_ERR_VALUE, "NULL argument");
-  const sp_layer_desc& d = *desc;
+static int validate_desc(const sp_layer_desc& d) {
   if (d.model_dim < 1 || d.hidden_dim < 1 || d.out_dim < 1)
     return fail(SP_ERR_SHAPE, "layer dims must be >= 1 (M=%lld H=%lld N=%lld)", (long long)d.model_dim,
                 (long long)d.hidden_dim, (long long)d.out_dim);
@@ -1442,35 +1486,41 @@ int sp_layer_create(const sp_layer_desc* desc, const void* w1t, const void* w3t,
   if (d.b1 < 0 || d.b2 < d.b1 || d.b2 > d.hidden_dim)
     return fail(SP_ERR_VALUE, "boundaries must satisfy 0 <= b1 <= b2 <= H (b1=%lld b2=%lld H=%lld)",
                 (long long)d.b1, (long long)d.b2, (long long)d.hidden_dim);
-  if (d.gated && !w3t) return fail(SP_ERR_VALUE, "gated layer needs w3t");
   if (d.act < 0 || d.act > 2) return fail(SP_ERR_VALUE, "unknown activation %d", d.act);
   if (d.wdtype != SP_F32 && d.wdtype != SP_BF16) return fail(SP_ERR_VALUE, "unknown weight dtype");
-  Context* C = ctx_or_null();
-  if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
-  std::lock_guard<std::mutex> g(C->mu);
-  auto L = std::make_unique<sp_layer>();
+  return SP_OK;
+}
+
+static void free_layer_memory(sp_layer* L) {
+  if (L->gg) cudaFree(L->gg);
+  L->gg = nullptr;
+  if (L->host && L->host_map_bytes) {
+    cudaHostUnregister(L->host);
+    munmap(L->host, L->host_map_bytes);
+  } else if (L->host) {
+    L->host_only ? free(L->host) : (void)cudaFreeHost(L->host);
+  }
+  L->host = nullptr;
+}
+
+// Validate, then place an empty layer (caller holds C->mu).
+static int new_layer(Context* C, const sp_layer_desc& d, std::unique_ptr<sp_layer>& L) {
+  SP_TRY(validate_desc(d));
+  L = std::make_unique<sp_layer>();
   L->d = d;
   L->device = C->device;
   L->esz = d.wdtype == SP_BF16 ? 2 : 4;
   L->ldm = round_up(d.model_dim, kPadElems);
   L->ldn = round_up(d.out_dim, kPadElems);
   L->host_only = C->host_only;
-  int st = pack_layer(L.get(), w1t, d.gated ? w3t : nullptr, w2);
-  if (st != SP_OK) {
-    if (L->gg) cudaFree(L->gg);
-    if (L->host && L->host_map_bytes) {
-    cudaHostUnregister(L->host);
-    munmap(L->host, L->host_map_bytes);
-  } else if (L->host) {
-    L->host_only ? free(L->host) : (void)cudaFreeHost(L->host);
-  }
-    return st;
-  }
-  if (C->host_only) {
-    *out = L.release();
-    return SP_OK;
-  }
-  if (L->max_chunk_bytes > C->ring_bytes) {
+  const int st = place_layer(L.get());
+  if (st != SP_OK) free_layer_memory(L.get());
+  return st;
+}
+
+// Grow the staging ring for the layer's largest chunk, hand the layer out.
+static int publish_layer(Context* C, std::unique_ptr<sp_layer>& L, sp_layer_t* out) {
+  if (!C->host_only && L->max_chunk_bytes > C->ring_bytes) {
     SP_CUDA(cudaDeviceSynchronize());
     for (int i = 0; i < kRingSlots; ++i) SP_TRY(C->ring[i].ensure(L->max_chunk_bytes));
     C->ring_bytes = C->ring[0].n;
@@ -1479,6 +1529,138 @@ int sp_layer_create(const sp_layer_desc* desc, const void* w1t, const void* w3t,
   return SP_OK;
 }
 
+int sp_layer_create(const sp_layer_desc* desc, const void* w1t, const void* w3t, const void* w2,
+                    sp_layer_t* out) {
+  if (!desc || !out || !w1t || !w2) return fail(SP_ERR_VALUE, "NULL argument");
+  if (desc->gated && !w3t) return fail(SP_ERR_VALUE, "gated layer needs w3t");
+  Context* C = ctx_or_null();
+  if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  std::lock_guard<std::mutex> g(C->mu);
+  std::unique_ptr<sp_layer> L;
+  SP_TRY(new_layer(C, *desc, L));
+  const int st = fill_rows(L.get(), w1t, desc->gated ? w3t : nullptr, w2);
+  if (st != SP_OK) {
+    free_layer_memory(L.get());
+    return st;
+  }
+  return publish_layer(C, L, out);
+}
+
+int sp_layer_image_sizes(sp_layer_t L, size_t* gg_bytes, size_t* host_bytes, int32_t* chunk_rows) {
+  if (!L) return fail(SP_ERR_VALUE, "NULL layer");
+  if (gg_bytes) *gg_bytes = L->gg_bytes;
+  if (host_bytes) *host_bytes = L->host_bytes;
+  if (chunk_rows) *chunk_rows = L->d.chunk_rows;
+  return SP_OK;
+}
+
+int sp_layer_export(sp_layer_t L, void* gg_dst, void* host_dst) {
+  if (!L) return fail(SP_ERR_VALUE, "NULL layer");
+  if (gg_dst && L->gg_bytes) SP_CUDA(cudaMemcpy(gg_dst, L->gg, L->gg_bytes, cudaMemcpyDeviceToHost));
+  if (host_dst && L->host_bytes) memcpy(host_dst, L->host, L->host_bytes);
+  return SP_OK;
+}
+
+int sp_layer_create_from_images(const sp_layer_desc* desc, const void* gg_img, size_t gg_bytes,
+                                const void* host_img, size_t host_bytes, sp_layer_t* out) {
+  if (!desc || !out) return fail(SP_ERR_VALUE, "NULL argument");
+  if (desc->chunk_rows <= 0) return fail(SP_ERR_VALUE, "images need the chunk_rows they were packed with");
+  Context* C = ctx_or_null();
+  if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  std::lock_guard<std::mutex> g(C->mu);
+  std::unique_ptr<sp_layer> L;
+  SP_TRY(new_layer(C, *desc, L));
+  int st = SP_OK;
+  if (L->gg_bytes != gg_bytes || L->host_bytes != host_bytes || (gg_bytes && !gg_img) || (host_bytes && !host_img))
+    st = fail(SP_ERR_SHAPE, "image sizes %zu/%zu do not match the layout %zu/%zu", gg_bytes, host_bytes,
+              L->gg_bytes, L->host_bytes);
+  if (st == SP_OK && gg_bytes && cudaMemcpy(L->gg, gg_img, gg_bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+    st = fail(SP_ERR_CUDA, "GG image upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+  if (st == SP_OK && host_bytes) memcpy(L->host, host_img, host_bytes);
+  if (st != SP_OK) {
+    free_layer_memory(L.get());
+    return st;
+  }
+  return publish_layer(C, L, out);
+}
+
+static int pread_all(int fd, void* dst, size_t n, uint64_t off, const char* path) {
+  char* p = static_cast<char*>(dst);
+  while (n > 0) {
+    const ssize_t r = pread(fd, p, std::min<size_t>(n, size_t(1) << 30), off_t(off));
+    if (r <= 0) return fail(SP_ERR_VALUE, "short read from %s at offset %llu", path, (unsigned long long)off);
+    p += r;
+    off += uint64_t(r);
+    n -= size_t(r);
+  }
+  return SP_OK;
+}
+
+int sp_layer_load_file(const sp_layer_desc* desc, const char* path, uint64_t gg_offset, size_t gg_bytes,
+                       uint64_t host_offset, size_t host_bytes, sp_layer_t* out) {
+  if (!desc || !path || !out) return fail(SP_ERR_VALUE, "NULL argument");
+  if (desc->chunk_rows <= 0) return fail(SP_ERR_VALUE, "images need the chunk_rows they were packed with");
+  Context* C = ctx_or_null();
+  if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return fail(SP_ERR_VALUE, "cannot open %s", path);
+  std::lock_guard<std::mutex> g(C->mu);
+  std::unique_ptr<sp_layer> L;
+  int st = new_layer(C, *desc, L);
+  if (st != SP_OK) {
+    close(fd);
+    return st;
+  }
+  if (L->gg_bytes != gg_bytes || L->host_bytes != host_bytes)
+    st = fail(SP_ERR_SHAPE, "image sizes %zu/%zu do not match the layout %zu/%zu", gg_bytes, host_bytes,
+              L->gg_bytes, L->host_bytes);
+  // host region: straight into the pinned (copy-engine visible) memory
+  if (st == SP_OK && host_bytes) st = pread_all(fd, L->host, host_bytes, host_offset, path);
+  // GG block: through a pinned bounce buffer, 8 MB at a time
+  if (st == SP_OK && gg_bytes) {
+    const size_t step = size_t(8) << 20;
+    void* bounce = nullptr;
+    if (cudaHostAlloc(&bounce, step, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      st = fail(SP_ERR_NOMEM, "cudaHostAlloc(8 MB) bounce buffer failed");
+    }
+    for (size_t o = 0; st == SP_OK && o < gg_bytes; o += step) {
+      const size_t n = std::min(step, gg_bytes - o);
+      st = pread_all(fd, bounce, n, gg_offset + o, path);
+      if (st == SP_OK && cudaMemcpy(static_cast<char*>(L->gg) + o, bounce, n, cudaMemcpyHostToDevice) != cudaSuccess)
+        st = fail(SP_ERR_CUDA, "GG image upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    if (bounce) cudaFreeHost(bounce);
+  }
+  close(fd);
+  if (st != SP_OK) {
+    free_layer_memory(L.get());
+    return st;
+  }
+  return publish_layer(C, L, out);
+}
+
+int sp_layer_reslice(sp_layer_t src, int64_t b1, int64_t b2, sp_layer_t* out) {
+  if (!src || !out) return fail(SP_ERR_VALUE, "NULL argument");
+  Context* C = ctx_or_null();
+  if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  std::lock_guard<std::mutex> g(C->mu);
+  sp_layer_desc d = src->d;
+  d.b1 = b1;
+  d.b2 = b2;
+  const int64_t H = d.hidden_dim, M = d.model_dim, N = d.out_dim;
+  std::vector<char> w1(size_t(H * M) * src->esz), w3(d.gated ? size_t(H * M) * src->esz : 0),
+      w2(size_t(H * N) * src->esz);
+  SP_TRY(gather_rows(src, w1.data(), d.gated ? w3.data() : nullptr, w2.data()));
+  std::unique_ptr<sp_layer> L;
+  SP_TRY(new_layer(C, d, L));
+  const int st = fill_rows(L.get(), w1.data(), d.gated ? w3.data() : nullptr, w2.data());
+  if (st != SP_OK) {
+    free_layer_memory(L.get());
+    return st;
+  }
+  return publish_layer(C, L, out);
+}
 int sp_layer_destroy(sp_layer_t L) {
   if (!L) return SP_OK;
   Context* C = ctx_or_null();
@@ -1487,13 +1669,7 @@ int sp_layer_destroy(sp_layer_t L) {
     cudaStreamSynchronize(C->s_comp);
     cudaStreamSynchronize(C->s_copy);
   }
-  if (L->gg) cudaFree(L->gg);
-  if (L->host && L->host_map_bytes) {
-    cudaHostUnregister(L->host);
-    munmap(L->host, L->host_map_bytes);
-  } else if (L->host) {
-    L->host_only ? free(L->host) : (void)cudaFreeHost(L->host);
-  }
+  free_layer_memory(L);
   delete L;
   return SP_OK;
 }

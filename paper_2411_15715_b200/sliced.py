@@ -151,7 +151,79 @@ class NativeLayer:
             C.byref(desc), a1.ctypes.data, None if a3 is None else a3.ctypes.data, a2.ctypes.data,
             C.byref(handle)))
         self._h = handle
-        self.chunk_rows = int(desc.chunk_rows)
+        cr = C.c_int32(0)  # the runtime picks chunk_rows when 0 was asked for
+        nat.check(nat.lib().sp_layer_image_sizes(handle, None, None, C.byref(cr)))
+        self.chunk_rows = int(cr.value)
+
+    @classmethod
+    def _adopt(cls, handle: C.c_void_p, model_dim: int, hidden_dim: int, out_dim: int, b1: int, b2: int,
+               gated: bool, activation: str, dtype: str, chunk_rows: int) -> "NativeLayer":
+        """Wrap a layer the runtime created (images, file, re-slice)."""
+        obj = cls.__new__(cls)
+        obj.model_dim, obj.hidden_dim, obj.out_dim = int(model_dim), int(hidden_dim), int(out_dim)
+        obj.b1, obj.b2 = int(b1), int(b2)
+        obj.gated, obj.activation, obj.dtype = bool(gated), _act_name(activation), dtype
+        obj.chunk_rows = int(chunk_rows)
+        obj._h = handle
+        return obj
+
+    def desc(self, b1: int | None = None, b2: int | None = None) -> "nat.LayerDesc":
+        return nat.LayerDesc(self.model_dim, self.hidden_dim, self.out_dim, int(self.gated),
+                             nat.ACT_CODES[self.activation], _dtype_code(self.dtype), self.chunk_rows,
+                             self.b1 if b1 is None else int(b1), self.b2 if b2 is None else int(b2))
+
+    def meta(self) -> dict:
+        """Everything besides the two images that recreates this layer."""
+        return {"model_dim": self.model_dim, "hidden_dim": self.hidden_dim, "out_dim": self.out_dim,
+                "b1": self.b1, "b2": self.b2, "gated": self.gated, "activation": self.activation,
+                "dtype": self.dtype, "chunk_rows": self.chunk_rows}
+
+    def image_sizes(self) -> tuple[int, int]:
+        gg, host = C.c_size_t(), C.c_size_t()
+        nat.check(nat.lib().sp_layer_image_sizes(self.handle, C.byref(gg), C.byref(host), None))
+        return gg.value, host.value
+
+    def export_images(self) -> tuple[np.ndarray, np.ndarray]:
+        """(GG image as laid out in HBM, pinned host region) as uint8 arrays."""
+        gg_n, host_n = self.image_sizes()
+        gg, host = np.empty(gg_n, dtype=np.uint8), np.empty(host_n, dtype=np.uint8)
+        nat.check(nat.lib().sp_layer_export(self.handle, gg.ctypes.data if gg_n else None,
+                                            host.ctypes.data if host_n else None))
+        return gg, host
+
+    @classmethod
+    def from_images(cls, meta: dict, gg: np.ndarray, host: np.ndarray, device: int | None = None) -> "NativeLayer":
+        nat.init(device)
+        obj = cls._adopt(None, **meta)
+        handle = C.c_void_p()
+        gg = np.ascontiguousarray(gg, dtype=np.uint8)
+        host = np.ascontiguousarray(host, dtype=np.uint8)
+        nat.check(nat.lib().sp_layer_create_from_images(
+            C.byref(obj.desc()), gg.ctypes.data if gg.size else None, gg.size,
+            host.ctypes.data if host.size else None, host.size, C.byref(handle)))
+        obj._h = handle
+        return obj
+
+    @classmethod
+    def load_file(cls, meta: dict, path: str, gg_offset: int, gg_bytes: int, host_offset: int, host_bytes: int,
+                  device: int | None = None) -> "NativeLayer":
+        nat.init(device)
+        obj = cls._adopt(None, **meta)
+        handle = C.c_void_p()
+        nat.check(nat.lib().sp_layer_load_file(C.byref(obj.desc()), str(path).encode(), int(gg_offset),
+                                               int(gg_bytes), int(host_offset), int(host_bytes), C.byref(handle)))
+        obj._h = handle
+        return obj
+
+    def reslice(self, b1: int, b2: int) -> "NativeLayer":
+        """A new layer with boundaries (b1, b2) from this one's weights."""
+        if not 0 <= b1 <= b2 <= self.hidden_dim:
+            raise ValueError(f"boundaries must satisfy 0 <= b1 <= b2 <= {self.hidden_dim}, got ({b1}, {b2})")
+        handle = C.c_void_p()
+        nat.check(nat.lib().sp_layer_reslice(self.handle, int(b1), int(b2), C.byref(handle)))
+        meta = self.meta()
+        meta.update(b1=int(b1), b2=int(b2))
+        return NativeLayer._adopt(handle, **meta)
 
     @property
     def handle(self) -> C.c_void_p:
@@ -472,6 +544,18 @@ class SlicedFFN:
     @property
     def block_widths(self) -> tuple[int, int, int]:
         return self.layer.block_widths
+
+    @classmethod
+    def from_layer(cls, layer: NativeLayer, rates: SlicingRates | None = None) -> "SlicedFFN":
+        obj = cls.__new__(cls)
+        obj.rates = rates
+        obj.layer = layer
+        return obj
+
+    def reslice(self, rates: SlicingRates) -> "SlicedFFN":
+        """Re-place under new rates (same floor rule as slice_weights)."""
+        b1, b2 = split_boundaries(self.layer.hidden_dim, rates)
+        return SlicedFFN.from_layer(self.layer.reslice(b1, b2), rates)
 
     def forward(self, x, n_g: int = 0, out=None):
         if not 0 <= n_g <= x.shape[0]:

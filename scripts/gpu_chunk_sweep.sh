@@ -1,0 +1,7 @@
+#!/bin/bash
+mkdir -p gpurun_out
+for mb in 8 16 4 8 16; do
+  echo "== SP_CHUNK_MB=$mb" >> gpurun_out/chunk_sweep.log
+  SP_CHUNK_MB=$mb timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value'],1), round(d['e2e']['value'],1), d['link'])" >> gpurun_out/chunk_sweep.log 2>&1
+done
+echo done
