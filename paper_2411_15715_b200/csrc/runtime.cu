@@ -145,7 +145,17 @@ struct Context {
   size_t ring_bytes = 0;
   int ring_next = 0;
   DevBuf ws;         // device workspace
-  PinnedBuf hpin;    // pinned host staging (ids/gates, x, y_cc, y)
+  // Pinned host staging (ids/gates, CSR, x, y_cc, y), two halves used by
+  // alternate forwards: a device-I/O forward returns before its copies and its
+  // finalize (which reads y_cc in place) have run, so the next forward must not
+  // write the same bytes.  hpin_done[i] is recorded after the last GPU use of
+  // half i; a forward waits on it before reusing the half.
+  PinnedBuf hpin[2];
+  cudaEvent_t hpin_done[2] = {nullptr, nullptr};
+  bool hpin_used[2] = {false, false};
+  int hpin_turn = 0;
+  cudaEvent_t ev_final = nullptr;  // after the previous forward's finalize (guards ws y_cc reuse)
+  bool final_recorded = false;
   PinnedBuf xroute;  // x read back for the MoE router (and reused by the CC blocks)
   DevBuf tc_partial;  // split-K partial tiles of the tensor-core GEMMs
   DevBuf tc_tickets;  // per-tile split tickets (zero, re-armed by the last split)
@@ -983,8 +993,11 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   std::vector<size_t> p_ycc(n_calls);
   for (int c = 0; c < n_calls; ++c) p_ycc[c] = palloc(size_t(calls[c].tokens) * N * 4);
   const size_t p_y = palloc(host_io ? size_t(T) * N * yel : 0);
-  SP_TRY(C->hpin.ensure(pin_off));
-  char* hp = static_cast<char*>(C->hpin.p);
+  const int hb = C->hpin_turn;
+  C->hpin_turn ^= 1;
+  if (C->hpin_used[hb]) SP_CUDA(cudaEventSynchronize(C->hpin_done[hb]));
+  SP_TRY(C->hpin[hb].ensure(pin_off));
+  char* hp = static_cast<char*>(C->hpin[hb].p);
 
   // ---- stream ordering against the caller ----
   SP_CUDA(cudaEventRecord(C->ev_user, user));
@@ -1242,8 +1255,11 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   // The tail runs on whichever thread finishes last: this one (GPU work all
   // enqueued) or the CC coordinator (CC block done) -- so finalize is enqueued
   // the moment both are ready, without a thread wake-up in between.
+  const bool prev_final = C->final_recorded;
   auto tail = [=]() -> int {
     if (ycc_copy) {
+      // the previous forward's finalize may still read the device y_cc buffers
+      if (prev_final) SP_CUDA(cudaStreamWaitEvent(C->s_aux, C->ev_final, 0));
       for (int c = 0; c < n_calls; ++c) {
         const int64_t Tcc = calls[c].tokens - calls[c].n_g;
         if (fa.c[c].y_cc != ws[c].ycc) continue;
@@ -1268,8 +1284,12 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       SP_CUDA(cudaMemcpyAsync(hp + p_y, dws + o_ydev, size_t(T) * N * yel, cudaMemcpyDeviceToHost, C->s_comp));
     else
       SP_CUDA(cudaEventRecord(C->ev_done, C->s_comp));
+    SP_CUDA(cudaEventRecord(C->ev_final, C->s_comp));
+    SP_CUDA(cudaEventRecord(C->hpin_done[hb], C->s_comp));
     return SP_OK;
   };
+  C->hpin_used[hb] = true;  // from here on the half's last GPU use is behind hpin_done[hb]
+  C->final_recorded = true;
   if (need_cc && cc_async) {
     SP_TRY(cc_join_with_tail(C, tail));
   } else {
@@ -1432,7 +1452,8 @@ int sp_init(int device, int host_threads) {
   SP_CUDA(cudaStreamCreateWithFlags(&C->s_comp, cudaStreamNonBlocking));
   SP_CUDA(cudaStreamCreateWithFlags(&C->s_copy, cudaStreamNonBlocking));
   SP_CUDA(cudaStreamCreateWithFlags(&C->s_aux, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&C->ev_user, &C->ev_x, &C->ev_ycc, &C->ev_done})
+  for (cudaEvent_t* e : {&C->ev_user, &C->ev_x, &C->ev_ycc, &C->ev_done, &C->ev_final, &C->hpin_done[0],
+                         &C->hpin_done[1]})
     SP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   for (int i = 0; i < kRingSlots; ++i) {
     SP_CUDA(cudaEventCreateWithFlags(&C->ev_copied[i], cudaEventDisableTiming));
@@ -1465,7 +1486,8 @@ int sp_shutdown(void) {
   }
   if (C->cc_thread.joinable()) C->cc_thread.join();
   cudaDeviceSynchronize();
-  for (cudaEvent_t e : {C->ev_user, C->ev_x, C->ev_ycc, C->ev_done}) cudaEventDestroy(e);
+  for (cudaEvent_t e : {C->ev_user, C->ev_x, C->ev_ycc, C->ev_done, C->ev_final, C->hpin_done[0], C->hpin_done[1]})
+    cudaEventDestroy(e);
   for (int i = 0; i < kRingSlots; ++i) {
     cudaEventDestroy(C->ev_copied[i]);
     cudaEventDestroy(C->ev_free[i]);
