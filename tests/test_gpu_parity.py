@@ -219,3 +219,23 @@ def test_prefill_moe_tensor_core_path(sp, torch):
     q = orc.bf16_round
     ref = orc.moe_forward(xq, [(q(a.T), q(b.T), q(c.T)) for a, b, c in ws], router, 2)
     assert orc.max_rel_error(got, ref) <= BF16_TOL
+
+
+@pytest.mark.parametrize("T", [1, 24])
+def test_back_to_back_device_forwards(sp, torch, T):
+    """Consecutive device-I/O forwards return before their GPU work (and the
+    finalize that reads the CC partial from pinned staging) has run: every
+    output must still be its own input's."""
+    from paper_2411_15715_b200.sliced import SlicedFFN
+
+    rng = np.random.default_rng(77 + T)
+    M, H = 512, 1536
+    w1t, w3t, w2t = (rng.standard_normal(s).astype(np.float32) / 16 for s in ((H, M), (H, M), (M, H)))
+    ffn = SlicedFFN(w1t, w2t, sp.SlicingRates(0.3, 0.3, 0.4), w3t=w3t, dtype="bf16", chunk_rows=128)
+    xs = [torch.from_numpy(rng.standard_normal((T, M)).astype(np.float32)).cuda().to(torch.bfloat16) for _ in range(8)]
+    ys = [ffn(x) for x in xs]  # no synchronisation in between
+    torch.cuda.synchronize()
+    q = orc.bf16_round
+    for x, y in zip(xs, ys):
+        ref = orc.dense_forward(q(x.float().cpu().numpy()), q(w1t.T), q(w2t.T), "silu", q(w3t.T))
+        assert orc.max_rel_error(y.float().cpu().numpy(), ref) <= BF16_TOL
