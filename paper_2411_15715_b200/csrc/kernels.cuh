@@ -574,6 +574,42 @@ __global__ void __launch_bounds__(kFinLanes * kFinGroups) finalize_kernel(FinalA
   }
 }
 
+// Same contract for many tokens with few slices (prefill: a handful of split-K
+// slices per call, hundreds of tokens): one thread per 4 output columns of one
+// token, the slices summed sequentially in slice order -- every thread busy and
+// every load a coalesced float4 (the slice-group layout above would leave 31 of
+// its 32 groups idle).
+__global__ void __launch_bounds__(256) finalize_rows_kernel(FinalArgs p) {
+  const int t = blockIdx.y;
+  const int n = (blockIdx.x * 256 + threadIdx.x) * 4;
+  if (n >= p.N) return;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int e = p.entry_start[t]; e < p.entry_start[t + 1]; ++e) {
+    const FinalCall& fc = p.c[p.entry_call[e]];
+    const int i = p.entry_row[e];
+    const int64_t stride = int64_t(fc.T_e) * p.N;
+    const float* base = fc.part + int64_t(i) * p.N + n;
+    float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < fc.S; ++s) {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(base + int64_t(s) * stride));
+      tot.x += a.x; tot.y += a.y; tot.z += a.z; tot.w += a.w;
+    }
+    if (fc.y_cc && i < fc.n_cc) {
+      const float4 c = *reinterpret_cast<const float4*>(fc.y_cc + int64_t(i) * p.N + n);
+      tot.x += c.x; tot.y += c.y; tot.z += c.z; tot.w += c.w;
+    }
+    const float gate = p.entry_gate[e];
+    acc.x += gate * tot.x; acc.y += gate * tot.y; acc.z += gate * tot.z; acc.w += gate * tot.w;
+  }
+  if (p.odtype == 1) {
+    __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.out) + int64_t(t) * p.N + n);
+    o[0] = __floats2bfloat162_rn(acc.x, acc.y);
+    o[1] = __floats2bfloat162_rn(acc.z, acc.w);
+  } else {
+    *reinterpret_cast<float4*>(static_cast<float*>(p.out) + int64_t(t) * p.N + n) = acc;
+  }
+}
+
 // Same contract for N % 4 != 0 (small test shapes): one thread per output element.
 __global__ void __launch_bounds__(256) finalize_scalar_kernel(FinalArgs p) {
   const int t = blockIdx.y;

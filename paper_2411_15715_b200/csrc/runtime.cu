@@ -508,7 +508,9 @@ static bool use_tc(const sp_layer* L, int64_t T) {
   if (L->d.wdtype != SP_BF16) return false;
   return g_tc_min_tokens_env > 0 ? T >= g_tc_min_tokens_env : T > max_token_tile(L->d.model_dim);
 }
-constexpr int kTcMaxSplits = 24;  // split-K output slices a resident tc block may use
+constexpr int kTcMaxSplits = 24;
+// finalize: per-token rows kernel up to this many slices per call, slice groups beyond
+constexpr int kFinRowsMaxSlices = 16;  // split-K output slices a resident tc block may use
 
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1243,6 +1245,8 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     fa.entry_gate = reinterpret_cast<const float*>(fa.entry_row + total_rows);
   }
   bool ycc_copy = false;
+  int max_slices = 0;
+  for (int c = 0; c < n_calls; ++c) max_slices = std::max(max_slices, ws[c].S);
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int64_t Tcc = calls[c].tokens - calls[c].n_g;
@@ -1270,7 +1274,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_ycc, 0));
     }
     GpuSpan span(C, C->s_comp, 2, SP_TRACE_MERGE, 0.0);
-    if (N % 4 == 0 && reinterpret_cast<uintptr_t>(fa.out) % 16 == 0) {
+    if (N % 4 == 0 && reinterpret_cast<uintptr_t>(fa.out) % 16 == 0 && max_slices <= kFinRowsMaxSlices) {
+      dim3 grid(unsigned((N / 4 + 255) / 256), unsigned(T));
+      finalize_rows_kernel<<<grid, 256, 0, C->s_comp>>>(fa);
+    } else if (N % 4 == 0 && reinterpret_cast<uintptr_t>(fa.out) % 16 == 0) {
       dim3 grid(unsigned((N + 4 * kFinLanes - 1) / (4 * kFinLanes)), unsigned(T));
       finalize_kernel<<<grid, kFinLanes * kFinGroups, 0, C->s_comp>>>(fa);
     } else {
