@@ -362,6 +362,8 @@ def run_ours(args):
         j = i % pool
         return moe(xs_host[j]) if host_io else moe(xs_dev[j])
 
+    per_step_wall = []  # host wall ms of every step, per timed region (outlier check)
+
     def timed(n, host_io=False, trace=False):
         if dist is not None:
             dist.barrier()
@@ -372,11 +374,14 @@ def run_ours(args):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         t0 = time.perf_counter()
+        ticks = [t0]
         for i in range(n):
             step(i, host_io)
+            ticks.append(time.perf_counter())
         b.record()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+        per_step_wall.append(np.diff(ticks) * 1e3)
         launches = nat.stats()["kernel_launches"] - l0
         spans = nat.trace_fetch() if trace else []
         if trace:
@@ -428,7 +433,8 @@ def run_ours(args):
     t_roof = max(gg_step_bytes / (hbm_peak * 1e9), cg_step_bytes / (link_peak * 1e9))
     cc_busy = sum(s["end_s"] - s["start_s"] for s in cc) / args.steps
     if args.trace_out and rank == 0:
-        Path(args.trace_out).write_text(json.dumps([s for s in spans if s["call"] < 4], indent=0))
+        keep = int(os.environ.get("SP_TRACE_KEEP_CALLS", "4"))
+        Path(args.trace_out).write_text(json.dumps([s for s in spans if s["call"] < keep], indent=0))
 
     if rank != 0:
         if dist is not None:
@@ -475,6 +481,9 @@ def run_ours(args):
         "clocks": clocks,
         "cpu_baseline": cpu,
         "wall_ms_per_step": wall_step * 1e3,
+        "step_wall_ms": {name: {"p50": float(np.percentile(w, 50)), "p90": float(np.percentile(w, 90)),
+                                "max": float(np.max(w))}
+                         for name, w in zip(("value", "e2e"), per_step_wall)},
     }
     print(json.dumps(line), flush=True)
     if dist is not None:

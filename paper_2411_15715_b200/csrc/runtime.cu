@@ -72,16 +72,37 @@ static inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * 
 // ---------------------------------------------------------------------------
 // device buffers
 
+// Growable device buffer.  Growth doubles (steady state never grows again) and,
+// given the stream that uses the buffer, is stream-ordered (cudaFreeAsync /
+// cudaMallocAsync): a plain cudaFree synchronises the whole device, i.e. waits
+// for every in-flight chunk copy -- a 10-30 ms stall inside a decode step.
 struct DevBuf {
   void* p = nullptr;
   size_t n = 0;
-  int ensure(size_t bytes) {
+  bool async = false;
+  int ensure(size_t bytes, cudaStream_t s = nullptr) {
     if (bytes <= n) return SP_OK;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-    const size_t want = std::max(bytes, size_t(1) << 20);
-    if (cudaMalloc(&p, want) != cudaSuccess) return fail(SP_ERR_NOMEM, "cudaMalloc(%zu) failed", want);
+    const size_t want = std::max({bytes, n * 2, size_t(1) << 20});
+    if (s) {
+      if (p) {
+        if (async) cudaFreeAsync(p, s);
+        else cudaFree(p);
+      }
+      p = nullptr;
+      n = 0;
+      if (cudaMallocAsync(&p, want, s) != cudaSuccess)
+        return fail(SP_ERR_NOMEM, "cudaMallocAsync(%zu) failed", want);
+      async = true;
+    } else {
+      if (p) {
+        if (async) cudaFreeAsync(p, 0);
+        else cudaFree(p);
+      }
+      p = nullptr;
+      n = 0;
+      if (cudaMalloc(&p, want) != cudaSuccess) return fail(SP_ERR_NOMEM, "cudaMalloc(%zu) failed", want);
+      async = false;
+    }
     n = want;
     return SP_OK;
   }
@@ -90,15 +111,19 @@ struct DevBuf {
   }
 };
 
+// Growable pinned host buffer.  cudaFreeHost synchronises the device, so a
+// grown-out buffer is retired (freed at destruction) instead of freed on the
+// spot; growth doubles, so the retired total stays below the live size.
 struct PinnedBuf {
   void* p = nullptr;
   size_t n = 0;
+  std::vector<void*> retired;
   int ensure(size_t bytes) {
     if (bytes <= n) return SP_OK;
-    if (p) cudaFreeHost(p);
+    const size_t want = std::max({bytes, n * 2, size_t(1) << 16});
+    if (p) retired.push_back(p);
     p = nullptr;
     n = 0;
-    const size_t want = std::max(bytes, size_t(1) << 16);
     if (cudaHostAlloc(&p, want, cudaHostAllocDefault) != cudaSuccess)
       return fail(SP_ERR_NOMEM, "cudaHostAlloc(%zu) failed", want);
     n = want;
@@ -106,6 +131,7 @@ struct PinnedBuf {
   }
   ~PinnedBuf() {
     if (p) cudaFreeHost(p);
+    for (void* r : retired) cudaFreeHost(r);
   }
 };
 
@@ -154,8 +180,7 @@ struct Context {
   cudaEvent_t hpin_done[2] = {nullptr, nullptr};
   bool hpin_used[2] = {false, false};
   int hpin_turn = 0;
-  cudaEvent_t ev_final = nullptr;  // after the previous forward's finalize (guards ws y_cc reuse)
-  bool final_recorded = false;
+  cudaEvent_t ev_ws = nullptr;  // on s_comp after this forward's workspace (re)allocation
   PinnedBuf xroute;  // x read back for the MoE router (and reused by the CC blocks)
   DevBuf tc_partial;  // split-K partial tiles of the tensor-core GEMMs
   DevBuf tc_tickets;  // per-tile split tickets (zero, re-armed by the last split)
@@ -478,6 +503,57 @@ static int launch_group(Context* C, const sp_layer* L, int tt, const FfnGroup& g
   return L->d.gated ? launch_tt<float, true>(C, tt, g, grid, s) : launch_tt<float, false>(C, tt, g, grid, s);
 }
 
+// ---- eager module loading ------------------------------------------------
+// CUDA loads kernels lazily (CUDA_MODULE_LOADING=LAZY is the default): the
+// first launch of each template instance loads it, which can hold the host
+// tens of ms and serialises against in-flight work.  With ~60 instances picked
+// by token count at run time, a new routing pattern in the middle of a decode
+// run paid that inside the step (measured: 55 ms outliers).  sp_init touches
+// every instance once and sets its shared-memory opt-in.
+template <typename K>
+static int preload(K kern, bool big_smem) {
+  cudaFuncAttributes a;
+  SP_CUDA(cudaFuncGetAttributes(&a, kern));
+  if (big_smem) SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+  return SP_OK;
+}
+template <typename WT, int TT, bool GATED>
+static int preload_ffn() {
+  SP_TRY(preload(ffn_block_kernel<WT, TT, GATED, 1>, true));
+  SP_TRY(preload(ffn_block_kernel<WT, TT, GATED, 2>, true));
+  return preload(ffn_block_kernel<WT, TT, GATED, 4>, true);
+}
+template <int NA, bool DOWN>
+static int preload_gemm() {
+  SP_TRY(preload(tc::gemm_kernel<16, NA, DOWN>, true));
+  SP_TRY(preload(tc::gemm_kernel<32, NA, DOWN>, true));
+  SP_TRY(preload(tc::gemm_kernel<64, NA, DOWN>, true));
+  SP_TRY(preload(tc::gemm_kernel<128, NA, DOWN>, true));
+  return preload(tc::gemm_kernel<256, NA, DOWN>, true);
+}
+static int preload_kernels() {
+  SP_TRY((preload_ffn<float, 1, false>()));
+  SP_TRY((preload_ffn<float, 2, false>()));
+  SP_TRY((preload_ffn<float, 4, false>()));
+  SP_TRY((preload_ffn<float, 1, true>()));
+  SP_TRY((preload_ffn<float, 2, true>()));
+  SP_TRY((preload_ffn<float, 4, true>()));
+  SP_TRY((preload_ffn<__nv_bfloat16, 1, false>()));
+  SP_TRY((preload_ffn<__nv_bfloat16, 2, false>()));
+  SP_TRY((preload_ffn<__nv_bfloat16, 4, false>()));
+  SP_TRY((preload_ffn<__nv_bfloat16, 1, true>()));
+  SP_TRY((preload_ffn<__nv_bfloat16, 2, true>()));
+  SP_TRY((preload_ffn<__nv_bfloat16, 4, true>()));
+  SP_TRY((preload_gemm<1, false>()));
+  SP_TRY((preload_gemm<2, false>()));
+  SP_TRY((preload_gemm<2, true>()));
+  SP_TRY(preload(finalize_kernel, false));
+  SP_TRY(preload(finalize_rows_kernel, false));
+  SP_TRY(preload(finalize_scalar_kernel, false));
+  SP_TRY(preload(tc::swiglu_reduce_kernel, false));
+  return preload(tc::gather_rows_bf16_kernel, false);
+}
+
 // One weight block applied to tokens [t0, t0 + T) of a call: partial slices
 // [slice0, slice0 + grid) of the call's partial buffer.
 struct BlockView {
@@ -559,11 +635,11 @@ static int launch_gemm_t(Context* C, const CUtensorMap& a0, const CUtensorMap& a
   const size_t smem = size_t(g.stages) * STAGE + 1024 + 256;
   if (g.ks > 1) {
     const size_t need = size_t(g.m_tiles) * g.t_tiles * g.ks * NA * NT * tc::BM * 4;
-    SP_TRY(C->tc_partial.ensure(need));
+    SP_TRY(C->tc_partial.ensure(need, s));
     g.partial = static_cast<float*>(C->tc_partial.p);
     const size_t tk = size_t(g.m_tiles) * g.t_tiles * 4;
     if (tk > C->tc_tickets.n) {
-      SP_TRY(C->tc_tickets.ensure(tk));
+      SP_TRY(C->tc_tickets.ensure(tk, s));
       SP_CUDA(cudaMemsetAsync(C->tc_tickets.p, 0, C->tc_tickets.n, s));
     }
     g.tickets = static_cast<int*>(C->tc_tickets.p);
@@ -633,7 +709,7 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
   if (up.ks > 1) {
     // split partials of the pre-activations, finished by swiglu_reduce_kernel
     up.zld = round_up(R, 4);
-    SP_TRY(C->tc_z.ensure(size_t(up.ks) * na * T * up.zld * 4));
+    SP_TRY(C->tc_z.ensure(size_t(up.ks) * na * T * up.zld * 4, s));
     up.z = static_cast<float*>(C->tc_z.p);
   }
   if (L->d.gated)
@@ -966,7 +1042,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   const size_t o_csr = dalloc(size_t(T + 1 + 3 * total_rows) * 4);
   const size_t o_xdev = dalloc(host_io ? size_t(T) * M * xel : 0);
   const size_t o_ydev = dalloc(host_io ? size_t(T) * N * yel : 0);
-  SP_TRY(C->ws.ensure(dev_off));
+  SP_TRY(C->ws.ensure(dev_off, C->s_comp));
+  // other streams touching ws (the aux stream's CC-partial copies) order after
+  // this point: the (stream-ordered) allocation and the previous forward's finalize
+  SP_CUDA(cudaEventRecord(C->ev_ws, C->s_comp));
   char* dws = static_cast<char*>(C->ws.p);
   for (int c = 0; c < n_calls; ++c) {
     ws[c].part = reinterpret_cast<float*>(dws + o_part[c]);
@@ -1259,11 +1338,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   // The tail runs on whichever thread finishes last: this one (GPU work all
   // enqueued) or the CC coordinator (CC block done) -- so finalize is enqueued
   // the moment both are ready, without a thread wake-up in between.
-  const bool prev_final = C->final_recorded;
   auto tail = [=]() -> int {
     if (ycc_copy) {
-      // the previous forward's finalize may still read the device y_cc buffers
-      if (prev_final) SP_CUDA(cudaStreamWaitEvent(C->s_aux, C->ev_final, 0));
+      // after ws's allocation and the previous forward's finalize (reads these buffers)
+      SP_CUDA(cudaStreamWaitEvent(C->s_aux, C->ev_ws, 0));
       for (int c = 0; c < n_calls; ++c) {
         const int64_t Tcc = calls[c].tokens - calls[c].n_g;
         if (fa.c[c].y_cc != ws[c].ycc) continue;
@@ -1291,12 +1369,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       SP_CUDA(cudaMemcpyAsync(hp + p_y, dws + o_ydev, size_t(T) * N * yel, cudaMemcpyDeviceToHost, C->s_comp));
     else
       SP_CUDA(cudaEventRecord(C->ev_done, C->s_comp));
-    SP_CUDA(cudaEventRecord(C->ev_final, C->s_comp));
     SP_CUDA(cudaEventRecord(C->hpin_done[hb], C->s_comp));
     return SP_OK;
   };
   C->hpin_used[hb] = true;  // from here on the half's last GPU use is behind hpin_done[hb]
-  C->final_recorded = true;
   if (need_cc && cc_async) {
     SP_TRY(cc_join_with_tail(C, tail));
   } else {
@@ -1459,7 +1535,7 @@ int sp_init(int device, int host_threads) {
   SP_CUDA(cudaStreamCreateWithFlags(&C->s_comp, cudaStreamNonBlocking));
   SP_CUDA(cudaStreamCreateWithFlags(&C->s_copy, cudaStreamNonBlocking));
   SP_CUDA(cudaStreamCreateWithFlags(&C->s_aux, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&C->ev_user, &C->ev_x, &C->ev_ycc, &C->ev_done, &C->ev_final, &C->hpin_done[0],
+  for (cudaEvent_t* e : {&C->ev_user, &C->ev_x, &C->ev_ycc, &C->ev_done, &C->ev_ws, &C->hpin_done[0],
                          &C->hpin_done[1]})
     SP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   for (int i = 0; i < kRingSlots; ++i) {
@@ -1470,6 +1546,7 @@ int sp_init(int device, int host_threads) {
   C->pool = std::make_unique<ThreadPool>(C->host_threads);
   Context* raw = C.get();
   C->cc_thread = std::thread([raw] { cc_coordinator(raw); });
+  SP_TRY(preload_kernels());
   if (env_int("SP_KSTAMPS", 0)) {
     SP_CUDA(cudaMalloc(&C->stamps, 4096 * 8 * sizeof(unsigned long long)));
     SP_CUDA(cudaMemset(C->stamps, 0, 4096 * 8 * sizeof(unsigned long long)));
@@ -1493,7 +1570,7 @@ int sp_shutdown(void) {
   }
   if (C->cc_thread.joinable()) C->cc_thread.join();
   cudaDeviceSynchronize();
-  for (cudaEvent_t e : {C->ev_user, C->ev_x, C->ev_ycc, C->ev_done, C->ev_final, C->hpin_done[0], C->hpin_done[1]})
+  for (cudaEvent_t e : {C->ev_user, C->ev_x, C->ev_ycc, C->ev_done, C->ev_ws, C->hpin_done[0], C->hpin_done[1]})
     cudaEventDestroy(e);
   for (int i = 0; i < kRingSlots; ++i) {
     cudaEventDestroy(C->ev_copied[i]);
