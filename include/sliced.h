@@ -173,7 +173,11 @@ typedef enum sp_trace_kind {
   SP_TRACE_CG_PRIME = 3, /* gpu: one streamed CC chunk for the n_g rows    */
   SP_TRACE_COPY = 4,     /* transfer: one chunk's host-to-device copy      */
   SP_TRACE_CC = 5,       /* cpu: CC block of one call on host threads      */
-  SP_TRACE_MERGE = 6     /* gpu: merge kernel                              */
+  SP_TRACE_MERGE = 6,    /* gpu: merge kernel                              */
+  SP_TRACE_ROUTE = 7,    /* host: MoE call entry -> dispatch (x read-back,
+                            routing, grouping)                             */
+  SP_TRACE_RETURN = 8    /* host: forward enqueue done -> return to caller
+                            (CC join, tail)                                */
 } sp_trace_kind;
 typedef struct sp_trace_record {
   int32_t index;  /* 1-based item index within its stream                */

@@ -30,6 +30,8 @@
 #include <vector>
 
 #include "../../include/sliced.h"
+#include <immintrin.h>
+
 #include "host_cc.h"
 #include "kernels.cuh"
 #include "gemm_tc.cuh"
@@ -159,6 +161,7 @@ struct Trace {
   int kslot_cur = -1;  // slot of the GpuSpan being enqueued, picked up by ffn_args
 };
 constexpr int kKSlots = 16384;
+constexpr int kTracePoolEvents = 8192;
 
 struct Context {
   int device = -1;
@@ -1304,7 +1307,8 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     if (next_copy < items.size()) SP_TRY(enqueue_copy());
   }
 
-  host_span(C, 0, SP_TRACE_LAUNCH, t_call, now_s(), 0.0);
+  const double t_enq_done = now_s();
+  host_span(C, 0, SP_TRACE_LAUNCH, t_call, t_enq_done, 0.0);
 
   // ---- finalize: reduce slices + CC partials + gates + cast ----
   // Small CC partials are read by finalize_kernel straight from pinned host
@@ -1385,6 +1389,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   } else {
     SP_CUDA(cudaStreamWaitEvent(user, C->ev_done, 0));
   }
+  host_span(C, 0, SP_TRACE_RETURN, t_enq_done, now_s(), 0.0);
   if (C->trace.on) ++C->trace.call;
   return SP_OK;
 }
@@ -1394,26 +1399,59 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
 // ---------------------------------------------------------------------------
 // MoE routing (host, fp64) and the one-call MoE layer
 
+// logits[t, e] = sum_m x[t, m] * router[m, e] in fp64, m ascending, one
+// multiply then one add per term -- the same IEEE operations whether the e loop
+// is scalar or 8-wide (fp contraction off, so no FMA changes the rounding).
+__attribute__((target("avx512f"), optimize("fp-contract=off"))) static void route_logits_avx512(
+    const float* router, int64_t M, int E, const void* x, int xdtype, double* logit) {
+  __m512d acc[8];
+  const int nv = E / 8;
+  for (int v = 0; v < nv; ++v) acc[v] = _mm512_setzero_pd();
+  for (int64_t m = 0; m < M; ++m) {
+    double xv;
+    if (xdtype == SP_BF16) {
+      const uint32_t u = uint32_t(static_cast<const uint16_t*>(x)[m]) << 16;
+      float f;
+      memcpy(&f, &u, 4);
+      xv = f;
+    } else {
+      xv = static_cast<const float*>(x)[m];
+    }
+    const __m512d xb = _mm512_set1_pd(xv);
+    const float* rrow = router + m * E;
+    for (int v = 0; v < nv; ++v)
+      acc[v] = _mm512_add_pd(acc[v], _mm512_mul_pd(xb, _mm512_cvtps_pd(_mm256_loadu_ps(rrow + 8 * v))));
+  }
+  for (int v = 0; v < nv; ++v) _mm512_storeu_pd(logit + 8 * v, acc[v]);
+}
+
+__attribute__((optimize("fp-contract=off"))) static void route_logits(const float* router, int64_t M, int E,
+                                                                      const void* x, int xdtype, double* logit) {
+  if (E % 8 == 0 && E <= 64 && host_has_avx512()) return route_logits_avx512(router, M, E, x, xdtype, logit);
+  for (int e = 0; e < E; ++e) logit[e] = 0.0;
+  for (int64_t m = 0; m < M; ++m) {
+    double xv;
+    if (xdtype == SP_BF16) {
+      const uint32_t u = uint32_t(static_cast<const uint16_t*>(x)[m]) << 16;
+      float f;
+      memcpy(&f, &u, 4);
+      xv = f;
+    } else {
+      xv = static_cast<const float*>(x)[m];
+    }
+    const float* rrow = router + m * E;
+    for (int e = 0; e < E; ++e) logit[e] += xv * double(rrow[e]);
+  }
+}
+
 static int moe_route(const float* router, int64_t M, int E, int k, const void* x, int xdtype, int64_t T,
                      int32_t* ids, float* gates) {
   if (E < 1 || k < 1 || k > E) return fail(SP_ERR_VALUE, "top_k must lie in [1, %d], got %d", E, k);
   std::vector<double> logit(static_cast<size_t>(E), 0.0);
   std::vector<int> order(static_cast<size_t>(E), 0);
+  const size_t xel = xdtype == SP_BF16 ? 2 : 4;
   for (int64_t t = 0; t < T; ++t) {
-    std::fill(logit.begin(), logit.end(), 0.0);
-    for (int64_t m = 0; m < M; ++m) {
-      double xv;
-      if (xdtype == SP_BF16) {
-        const uint32_t u = uint32_t(static_cast<const uint16_t*>(x)[t * M + m]) << 16;
-        float f;
-        memcpy(&f, &u, 4);
-        xv = f;
-      } else {
-        xv = static_cast<const float*>(x)[t * M + m];
-      }
-      const float* rrow = router + m * E;
-      for (int e = 0; e < E; ++e) logit[e] += xv * double(rrow[e]);
-    }
+    route_logits(router, M, E, static_cast<const char*>(x) + size_t(t) * M * xel, xdtype, logit.data());
     for (int e = 0; e < E; ++e) order[e] = e;
     // k largest, ties to the lower expert id (a stable descending sort)
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return logit[a] > logit[b]; });
@@ -1439,6 +1477,7 @@ static int moe_forward(Context* C, const sp_layer_t* layers, int E, const float*
   const int64_t M = any->d.model_dim;
   const size_t xel = xdtype == SP_BF16 ? 2 : 4;
   const bool host_io = flags & SP_IO_HOST;
+  const double t_route0 = now_s();
   // one read of x serves the router and every CC block
   const void* xh = x;
   if (!host_io) {
@@ -1448,7 +1487,9 @@ static int moe_forward(Context* C, const sp_layer_t* layers, int E, const float*
     SP_CUDA(cudaMemcpyAsync(C->xroute.p, x, size_t(T) * M * xel, cudaMemcpyDeviceToHost, C->s_aux));
     SP_CUDA(cudaStreamSynchronize(C->s_aux));
     xh = C->xroute.p;
+    host_span(C, 0, SP_TRACE_ROUTE, t_route0, now_s(), double(size_t(T) * M * xel));  // x read-back
   }
+  const double t_route1 = now_s();
   std::vector<int32_t> ids(static_cast<size_t>(T * k));
   std::vector<float> gates(static_cast<size_t>(T * k));
   SP_TRY(moe_route(router, M, E, k, xh, xdtype, T, ids.data(), gates.data()));
@@ -1476,6 +1517,7 @@ static int moe_forward(Context* C, const sp_layer_t* layers, int E, const float*
     return SP_OK;
   }
   if (int(calls.size()) > kMaxCalls) return fail(SP_ERR_VALUE, "%zu active experts exceed %d", calls.size(), kMaxCalls);
+  host_span(C, 0, SP_TRACE_ROUTE, t_route1, now_s(), 0.0);  // routing + grouping
   return forward_batch(C, calls.data(), int(calls.size()), x, xdtype, T, y, ydtype, flags, user,
                        host_io ? nullptr : xh);
 }
@@ -1864,6 +1906,13 @@ int sp_trace_enable(int on) {
   tr.kspan_next = 0;
   tr.kslot_cur = -1;
   if (tr.on) {
+    // events for the spans of the traced region, created up front: cudaEventCreate
+    // inside a forward costs microseconds per span on the launching thread
+    while (tr.pool.size() < size_t(kTracePoolEvents)) {
+      cudaEvent_t e = nullptr;
+      SP_CUDA(cudaEventCreate(&e));
+      tr.pool.push_back(e);
+    }
     if (!tr.kspan) SP_CUDA(cudaMalloc(&tr.kspan, size_t(2) * kKSlots * sizeof(unsigned long long)));
     SP_CUDA(cudaMemset(tr.kspan, 0xff, size_t(kKSlots) * sizeof(unsigned long long)));
     SP_CUDA(cudaMemset(tr.kspan + kKSlots, 0, size_t(kKSlots) * sizeof(unsigned long long)));

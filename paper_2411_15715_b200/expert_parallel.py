@@ -21,7 +21,7 @@ from typing import Callable, Mapping, Sequence
 import numpy as np
 
 from .errors import ShapeMismatch
-from .sliced import CallSpec, forward_calls, moe_forward, route_topk
+from .sliced import CallSpec, MoEDispatch, forward_calls, route_topk
 
 
 def owner_of(expert: int, world: int) -> int:
@@ -78,6 +78,7 @@ class ExpertParallelMoE:
                        else self.router_w.shape[0])
         self.out_dim = int(out_dim)
         self.local_forward = local_forward or self._gpu_local_forward
+        self._dispatch = None
 
     def _gpu_local_forward(self, plan, x):
         calls = [CallSpec(self.experts[e].layer, rows, gates) for e, rows, gates in plan]
@@ -92,8 +93,10 @@ class ExpertParallelMoE:
 
         if x_host is None and self.local_forward == self._gpu_local_forward:
             # native routing + dispatch: one read-back of x serves router and CC blocks
-            layers = [self.experts[e].layer if e in self.experts else None for e in range(self.n_experts)]
-            y = moe_forward(layers, self.router_w, self.top_k, x)
+            if self._dispatch is None:
+                layers = [self.experts[e].layer if e in self.experts else None for e in range(self.n_experts)]
+                self._dispatch = MoEDispatch(layers, self.router_w, self.top_k)
+            y = self._dispatch(x)
             if not isinstance(y, torch.Tensor):
                 y = torch.as_tensor(np.ascontiguousarray(y))
             return self._reduce(y)

@@ -30,7 +30,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .schedule import SlicingRates
-from .sliced import SlicedFFN, moe_forward
+from .sliced import MoEDispatch, SlicedFFN
 
 
 @dataclass
@@ -84,6 +84,8 @@ class SlicedMixtral:
             for _ in range(cfg.experts)])
         self.moe_sets = [make(d) for d in range(cfg.distinct)]
         self.routers = [rng.standard_normal((M, cfg.experts)) / math.sqrt(M) for _ in range(cfg.distinct)]
+        self.dispatch = [MoEDispatch([e.layer for e in self.moe_sets[d]], self.routers[d], cfg.top_k)
+                         for d in range(cfg.distinct)] if self.moe_sets and self.moe_sets[0] else []
         kv_shape = (cfg.layers, 2, 1, cfg.kv_heads, cfg.max_seq, hd)
         self.kv = torch.zeros(kv_shape, device=dev, dtype=tdt)
         pos = torch.arange(cfg.max_seq, device=dev, dtype=torch.float32)
@@ -136,7 +138,7 @@ class SlicedMixtral:
         return x
 
     def _moe(self, d: int, h, out=None):
-        return moe_forward([e.layer for e in self.moe_sets[d]], self.routers[d], self.cfg.top_k, h, out)
+        return self.dispatch[d](h, out)
 
     # -- CUDA-graph decode ------------------------------------------------------
     # Per layer the torch part (residual add of the previous MoE output, RMSNorm,

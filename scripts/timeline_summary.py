@@ -21,4 +21,6 @@ for c in sorted(by):
           f"copy {us(f({'copy'}, 'start_s', min)):7.1f}-{us(f({'copy'}, 'end_s', max)):7.1f} "
           f"({len(cps)} x, {byt / busy / 1e9 if busy else 0:5.1f} GB/s busy, gaps sum {sum(gaps) * 1e6:6.1f}) | "
           f"cg end {us(f({'cg'}, 'end_s', max)):7.1f} | cc {us(f({'cc'}, 'start_s', min)):7.1f}-{us(f({'cc'}, 'end_s', max)):7.1f} | "
-          f"merge {us(f({'merge'}, 'start_s', min)):7.1f}-{us(f({'merge'}, 'end_s', max)):7.1f}")
+          f"merge {us(f({'merge'}, 'start_s', min)):7.1f}-{us(f({'merge'}, 'end_s', max)):7.1f} | "
+          f"route {us(f({'route'}, 'start_s', min)):7.1f}-{us(f({'route'}, 'end_s', max)):7.1f} | "
+          f"return {us(f({'return'}, 'start_s', min)):7.1f}-{us(f({'return'}, 'end_s', max)):7.1f}")
