@@ -19,6 +19,8 @@ Keys of the JSON line (rank 0):
   roofline GG ffn_block launch (dominant HBM kernel) achieved GB/s vs MEASURED_PEAKS
   link     CG copy GB/s vs the measured link, and the step roofline
            t_roof = max(GG bytes / HBM, CG bytes / link) / measured step
+           (north-star definition), plus the bound that includes the host:
+           max(t_roof, CC bytes / fitted in-situ CC rate)
   cpu_baseline  the reference algorithm (oracle/sliced_forward.py, fp64 numpy,
            slicing_kernel.py:97-124) on the host cores, bounded sample
 
@@ -114,6 +116,12 @@ def load_profile(path):
     if p.exists():
         return costs.load_profile(p), str(p.relative_to(ROOT) if p.is_relative_to(ROOT) else p)
     return costs.profile_from_dict(FALLBACK_DECODE), "fallback (b200_profile.FALLBACK_DECODE)"
+
+
+def sp_precision_fp16():
+    from paper_2411_15715_b200.costs import Precision
+
+    return Precision.FP16
 
 
 def decode_profile_for(path, t_expert: int) -> str:
@@ -432,6 +440,11 @@ def run_ours(args):
     cg_step_bytes = cp_bytes / args.steps
     t_roof = max(gg_step_bytes / (hbm_peak * 1e9), cg_step_bytes / (link_peak * 1e9))
     cc_busy = sum(s["end_s"] - s["start_s"] for s in cc) / args.steps
+    # the host side of the step: CC bytes at the profile's fitted (in-situ) CC rate
+    cc_step_bytes = sum(s["bytes"] for s in cc) / args.steps
+    g16 = profile.gemm.get(sp_precision_fp16()) if profile.gemm else None
+    cc_rate = 2.0 / g16.cpu.beta if g16 is not None and g16.cpu and g16.cpu.beta else None
+    t_host = max(t_roof, cc_step_bytes / cc_rate) if cc_rate else None
     if args.trace_out and rank == 0:
         keep = int(os.environ.get("SP_TRACE_KEEP_CALLS", "4"))
         Path(args.trace_out).write_text(json.dumps([s for s in spans if s["call"] < keep], indent=0))
@@ -476,7 +489,10 @@ def run_ours(args):
                  "cg_GBps_over_step": cg_step_bytes / step_s / 1e9, "link_peak_GBps": link_peak,
                  "frac_over_step": (cg_step_bytes / step_s / 1e9) / link_peak if link_peak else None,
                  "step_roofline_s": t_roof, "step_roofline_frac": t_roof / step_s if step_s else None,
-                 "cc_host_s_per_step": cc_busy},
+                 "cc_host_s_per_step": cc_busy,
+                 "cc_rate_GBps_fitted": cc_rate / 1e9 if cc_rate else None,
+                 "step_bound_with_cc_s": t_host,
+                 "step_bound_with_cc_frac": t_host / step_s if t_host and step_s else None},
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": cpu,

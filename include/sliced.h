@@ -199,6 +199,10 @@ int sp_trace_fetch(sp_trace_record* out, int* n);
 /* Kernels launched and bytes copied host-to-device by the library so far. */
 int sp_stats(uint64_t* kernel_launches, uint64_t* h2d_bytes);
 
+/* fp32 -> bf16 bit patterns, round to nearest even (the host activation cast
+ * of the bf16 path; single-threaded AVX-512, no framework threads). */
+int sp_round_bf16(const float* src, uint16_t* dst, int64_t n);
+
 /* Pinned host buffer helpers (cudaHostAlloc; avoids torch's caching host
  * allocator rounding). */
 int sp_host_alloc(size_t bytes, void** ptr);

@@ -97,6 +97,7 @@ SIGNATURES = {
     "sp_stats": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "sp_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "sp_host_free": (C.c_int, [C.c_void_p]),
+    "sp_round_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
 }
 
 _lib = None
@@ -121,6 +122,11 @@ def lib():
                 fn.argtypes = args
             _lib = handle
         return _lib
+
+
+def available() -> bool:
+    """True when libsliced.so is built (host-side helpers need no device)."""
+    return _lib is not None or LIB_PATH.exists()
 
 
 def check(status: int) -> None:

@@ -1890,6 +1890,40 @@ int sp_cc_forward_host(sp_layer_t L, const void* x, int xdtype, int64_t T, float
   return SP_OK;
 }
 
+// fp32 -> bf16 bit patterns, round to nearest even: u + 0x7fff + ((u >> 16) & 1),
+// the same integer arithmetic as the Python fallback (NaNs are not special-cased).
+// Native so host activations never go through a multi-threaded framework cast,
+// whose spinning worker threads steal the cores the CC block runs on.
+__attribute__((target("avx512f,avx512bw"))) static void round_bf16_avx512(const float* src, uint16_t* dst,
+                                                                           int64_t n) {
+  const __m512i bias = _mm512_set1_epi32(0x7fff), one = _mm512_set1_epi32(1);
+  int64_t i = 0;
+  for (; i + 16 <= n; i += 16) {
+    __m512i u = _mm512_castps_si512(_mm512_loadu_ps(src + i));
+    u = _mm512_add_epi32(u, _mm512_add_epi32(bias, _mm512_and_si512(_mm512_srli_epi32(u, 16), one)));
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), _mm512_cvtepi32_epi16(_mm512_srli_epi32(u, 16)));
+  }
+  for (; i < n; ++i) {
+    uint32_t u;
+    memcpy(&u, src + i, 4);
+    dst[i] = uint16_t((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+  }
+}
+
+int sp_round_bf16(const float* src, uint16_t* dst, int64_t n) {
+  if (n < 0 || (n > 0 && (!src || !dst))) return fail(SP_ERR_VALUE, "NULL argument");
+  if (host_has_avx512()) {
+    round_bf16_avx512(src, dst, n);
+    return SP_OK;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t u;
+    memcpy(&u, src + i, 4);
+    dst[i] = uint16_t((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+  }
+  return SP_OK;
+}
+
 int sp_trace_enable(int on) {
   Context* C = ctx_or_null();
   if (!C || C->host_only) return fail(SP_ERR_STATE, "sp_init(device) has not been called");

@@ -75,10 +75,12 @@ def split_boundaries(hidden: int, rates: SlicingRates) -> tuple[int, int]:
 def to_bf16_bits(a: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even float -> bfloat16 bit patterns (uint16)."""
     f = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
-    torch = _maybe_torch()
-    if torch is not None and f.size >= (1 << 16):
-        # torch's multi-threaded RNE cast (30x faster than the numpy form below on a prompt)
-        return torch.from_numpy(f).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    if f.size >= 4096 and nat.available():
+        # native AVX-512 cast (~50x faster than the numpy form below on a prompt); not
+        # torch's: its spinning OpenMP workers would steal the CC block's cores
+        out = np.empty(f.shape, dtype=np.uint16)
+        nat.check(nat.lib().sp_round_bf16(f.ctypes.data, out.ctypes.data, f.size))
+        return out
     u = f.view(np.uint32).astype(np.uint64)
     u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
     return u

@@ -140,3 +140,15 @@ def test_moe_router_matches_oracle():
     # exact ties go to the lower expert id
     ids, gates = moe_route(np.ones((1, 4), np.float32), np.ones((4, 6), np.float32), 2)
     assert ids.tolist() == [[0, 1]] and np.allclose(gates, 0.5)
+
+
+def test_native_bf16_cast_matches_numpy_rule():
+    """sp_round_bf16 (host activation cast) == the integer RNE rule, bit for bit."""
+    from paper_2411_15715_b200.sliced import to_bf16_bits
+
+    rng = np.random.default_rng(9)
+    x = (rng.standard_normal(70001) * rng.choice([1e-40, 1e-3, 1.0, 1e30], 70001)).astype(np.float32)
+    x[:6] = [1.00390625, 1.01171875, -3.0e38, 0.0, np.inf, -np.inf]
+    u = x.view(np.uint32).astype(np.uint64)
+    ref = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    assert np.array_equal(to_bf16_bits(x), ref)
