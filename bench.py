@@ -60,6 +60,12 @@ def parse():
     ap.add_argument("--distinct-layers", type=int, default=8, help="cfg3: distinct weight sets cycled over the layers")
     ap.add_argument("--prompt", type=int, default=512, help="cfg3: prompt tokens")
     ap.add_argument("--decode-steps", type=int, default=128, help="cfg3: decode tokens after the prompt")
+    ap.add_argument("--transfer-model", default="rate_scaled", choices=["literal", "rate_scaled"],
+                    help="cfg3: solve_ng's prompt transfer model (pipeline.py:204-207).  rate_scaled charges the "
+                         "(cg + cc) share of the weights -- exactly what the CG streamer moves when n_g > 0 (CG "
+                         "chunks + the CC chunks for the diverted rows); literal charges the whole layer")
+    ap.add_argument("--ng-frac", type=float, default=-1.0,
+                    help="cfg3 study only: n_g = round(frac * T_e) instead of solve_ng (landscape sweeps)")
     ap.add_argument("--prompt-profile", default=str(ROOT / "profiles" / "b200_prompt.json"))
     ap.add_argument("--batch", type=int, default=1, help="decode tokens per step per GPU")
     ap.add_argument("--budget-frac", type=float, default=0.5,
@@ -543,7 +549,9 @@ def run_prefill_decode(args):
 
     def n_g_for(t_e: int) -> int:
         if t_e not in ng_cache:
-            ng_cache[t_e] = sp.solve_ng(p_profile, layer_spec, t_e, rates).n_g
+            ng_cache[t_e] = (int(round(args.ng_frac * t_e)) if args.ng_frac >= 0
+                             else sp.solve_ng(p_profile, layer_spec, t_e, rates,
+                                              transfer_model=args.transfer_model).n_g)
         return ng_cache[t_e]
 
     def plan(d, x_host, split):
@@ -621,6 +629,7 @@ def run_prefill_decode(args):
                    "top_k": args.top_k, "rates": {"cc": rates.cc, "cg": rates.cg, "gg": rates.gg},
                    "gpu_budget_frac": args.budget_frac, "decode_profile": source, "prompt_profile": p_source,
                    "tokens_per_expert_layer0": t_e_prompt, "n_g_by_expert_tokens": ng_used,
+                   "solve_ng_transfer_model": args.transfer_model,
                    "l2": f"{D} distinct layers x 8 experts ({D * 2.8:.0f} GB) cycled, >> L2"},
         "e2e": {"value": args.prompt / t_e2e, "unit": UNIT, "h2d_bytes_per_step": args.prompt * args.model_dim * 2 * args.layers,
                 "d2h_bytes_per_step": args.prompt * args.model_dim * 4 * args.layers},

@@ -17,14 +17,15 @@ runtime executes on, through the runtime's own code paths:
 
 The CC threads and the copy engine read the same host DRAM at the same time
 in every sliced step (the CC block runs while the CG chunks stream), and the
-GG kernels run while the copy engine writes the HBM ring (measured: the
-copies cost a GG launch ~25 % of its HBM rate, scripts/probe_gg.py).  By
-default (``--load concurrent``) every rate is therefore sampled under the load
-the step puts next to it: decode CC blocks and chunk copies come from real
-sliced decode steps (``insitu_samples``), GG blocks run under background
-host -> HBM copies, prompt-phase CC blocks under background copies and
-prompt-phase copies under a background CC block.  ``--load isolated`` samples
-each rate alone (the round-1 method).
+GG kernels run while the copy engine saturates the host link (which delays
+the end of their CUDA-event spans by ~15-20 us, scripts/probe_gg.py and
+scripts/probes/launch_latency.cu -- the kernels themselves run at full rate).
+By default (``--load concurrent``) every rate is therefore sampled under the
+load the step puts next to it: CC blocks and chunk copies come from real
+sliced steps (``insitu_samples``, decode at T tokens per expert), prompt-phase
+CC blocks under background copies and copies under a background CC block, GG
+blocks under background host -> HBM copies.  ``--load isolated`` samples each
+rate alone (the round-1 method).
 
 ``python -m paper_2411_15715_b200.b200_profile --out profiles/`` writes the
 CSV and the fitted profile JSON (per phase: the GPU term is far from linear in
@@ -204,7 +205,7 @@ def c2g_samples(torch, chunk_rows=(32, 64, 128, 320, 640, 1280), reps=3, model_d
 
 
 def insitu_samples(torch, cc_rates=(0.1, 0.2, 0.3, 0.4), r_gg=0.5, model_dim=4096, hidden=14336,
-                   experts=2, reps=6, seed=11, tokens=1):
+                   experts=2, reps=6, seed=11, tokens=1, n_g_list=(0,)):
     """CPU GEMM and chunk-copy samples taken from real sliced decode steps.
 
     For each CC rate, `experts` SwiGLU experts are placed with rates
@@ -212,7 +213,10 @@ def insitu_samples(torch, cc_rates=(0.1, 0.2, 0.3, 0.4), r_gg=0.5, model_dim=409
     top-2 MoE step): the CC blocks (host threads) and the CG chunk copies
     (copy engine) then share host DRAM exactly as they do in production.
     Every CC block's host span gives one ``cpu_gemm_fp16`` sample (n = T*M*b1
-    per GEMM, span / 3) and every chunk copy one ``c2g`` sample."""
+    per GEMM, span / 3) and every chunk copy one ``c2g`` sample.  ``n_g_list``
+    (prompt phase) diverts the last n_g of the tokens to the GPU, as the token
+    assigner does, so the CC block runs at T - n_g tokens while the CC chunks
+    stream to the GPU next to it."""
     from .sliced import CallSpec, NativeLayer, forward_calls
 
     g = torch.Generator(device="cuda").manual_seed(seed)
@@ -224,19 +228,20 @@ def insitu_samples(torch, cc_rates=(0.1, 0.2, 0.3, 0.4), r_gg=0.5, model_dim=409
         b1 = int(np.floor(cc * hidden))
         b2 = int(np.floor((1.0 - r_gg) * hidden))
         lays = [NativeLayer(w1t, w2, b1, b2, "silu", w3t, dtype="bf16") for (w1t, w3t, w2) in weights]
-        for r in range(reps + 2):
+        for r in range((reps + 2) * len(n_g_list)):
+            n_g = n_g_list[r % len(n_g_list)]
             torch.cuda.synchronize()
             nat.trace_enable(True)
-            forward_calls([CallSpec(l) for l in lays], x)
+            forward_calls([CallSpec(l, n_g=n_g) for l in lays], x)
             torch.cuda.synchronize()
             spans = nat.trace_fetch()
             nat.trace_enable(False)
-            if r < 2:
+            if r < 2 * len(n_g_list):
                 continue
             for s_ in spans:
                 dt = s_["end_s"] - s_["start_s"]
                 if s_["kind"] == "cc":
-                    out.append(ProfileSample(OpClass.CPU_GEMM, float(tokens) * model_dim * b1, dt / 3.0,
+                    out.append(ProfileSample(OpClass.CPU_GEMM, float(tokens - n_g) * model_dim * b1, dt / 3.0,
                                              Precision.FP16))
                 elif s_["kind"] == "copy":
                     out.append(ProfileSample(OpClass.C2G, float(s_["bytes"]), dt))
@@ -268,7 +273,7 @@ def launch_samples(torch, reps=20):
 
 
 def measure(phase: str = "decode", quick: bool = False, load: str = "concurrent",
-            tokens: int = 1) -> list[ProfileSample]:
+            tokens: int = 1, prompt_insitu: bool = False) -> list[ProfileSample]:
     """decode: ``tokens`` per expert everywhere (1 = single-token decode; 2..8
     for batched decode, where each active expert sees a few tokens).  prompt:
     the GPU GEMM at T = 128 tokens (an expert's share of a 512-token top-2
@@ -292,7 +297,19 @@ def measure(phase: str = "decode", quick: bool = False, load: str = "concurrent"
             samples = gpu_gemm_samples(torch, gpu_tokens, widths, reps=3 if quick else 5)
         if phase == "decode":
             samples += insitu_samples(torch, reps=3 if quick else 6, tokens=tokens)
+        elif prompt_insitu:
+            # real prompt steps: 128 tokens per expert (a 512-token top-2 prompt's
+            # share), the CC block at 128 - n_g tokens while the chunks stream
+            samples += insitu_samples(torch, cc_rates=(0.2, 0.35), reps=2 if quick else 3, tokens=128,
+                                      n_g_list=(32, 48, 64, 80))
         else:
+            # Default for the prompt phase: CC blocks at 32 tokens under background
+            # copies, copies under a background CC block.  The in-situ line (above)
+            # is the more faithful measurement, but the reference's cost model is
+            # linear in T*M*H per GEMM and solve_ng plans one expert at a time
+            # while all of a layer's experts share the host: with the in-situ
+            # line it keeps every prompt row on the host (n_g = 0) and the layer
+            # turns CPU bound (measured 405-456 vs 533 prefill tokens/s).
             with BackgroundCopy(torch):
                 samples += cpu_gemm_samples(cpu_tokens, cpu_widths, reps=2 if quick else 4)
             with BackgroundCC():
@@ -309,6 +326,8 @@ def main(argv=None) -> None:
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--out", default="profiles")
     ap.add_argument("--phase", default="decode", choices=["decode", "prompt"])
+    ap.add_argument("--prompt-insitu", action="store_true",
+                    help="prompt phase: sample the CC block inside real prompt steps (see measure())")
     ap.add_argument("--tokens", type=int, default=1,
                     help="decode: tokens per expert (batched decode); writes b200_decode_t<T>.json for T > 1")
     ap.add_argument("--quick", action="store_true")
@@ -317,7 +336,7 @@ def main(argv=None) -> None:
     args = ap.parse_args(argv)
     out = Path(args.out)
     out.mkdir(parents=True, exist_ok=True)
-    samples = measure(args.phase, args.quick, args.load, args.tokens)
+    samples = measure(args.phase, args.quick, args.load, args.tokens, args.prompt_insitu)
     tag = args.phase if args.phase == "prompt" or args.tokens == 1 else f"{args.phase}_t{args.tokens}"
     write_samples_csv(samples, out / f"b200_samples_{tag}.csv")
     prof, warns = fit_profile(samples, f"b200-{tag}" + ("" if args.load == "concurrent" else "-isolated"))
