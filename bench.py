@@ -599,6 +599,18 @@ def run_prefill_decode(args):
     clk.stop()
     ng_used = {t: n for t, n in sorted(ng_cache.items())}
     t_e_prompt = sorted({len(c.token_ids) for c in prompt_plans[0]})
+    # one traced prefill: the Y_cc transfer measured next to the reference's model of it
+    nat.trace_enable(True)
+    prefill()
+    torch.cuda.synchronize()
+    pspans = nat.trace_fetch()
+    nat.trace_enable(False)
+    ycc = [s for s in pspans if s["kind"] == "ycc"]
+    ycc_meas = sum(s["end_s"] - s["start_s"] for s in ycc) / args.layers
+    ycc_model = sum(sp.cc_result_transfer_time(p_profile, layer_spec,
+                                               sp.Workload(tokens=len(c.token_ids) - c.n_g, phase=sp.Phase.PROMPT),
+                                               rates, bytes_per_activation=4.0)
+                    for c in prompt_plans[0]) if hasattr(sp, "cc_result_transfer_time") else None
     if args.trace_out:
         nat.trace_enable(True)
         prefill()
@@ -634,6 +646,10 @@ def run_prefill_decode(args):
         "e2e": {"value": args.prompt / t_e2e, "unit": UNIT, "h2d_bytes_per_step": args.prompt * args.model_dim * 2 * args.layers,
                 "d2h_bytes_per_step": args.prompt * args.model_dim * 4 * args.layers},
         "gpu_launches": launches, "clocks": clk.summary(),
+        "ycc_transfer": {"measured_ms_per_layer": ycc_meas * 1e3,
+                         "model_ms_per_layer": ycc_model * 1e3 if ycc_model is not None else None,
+                         "note": "CC partials host->HBM (pipeline.py:367-383 cc_result_transfer_time, fp32 "
+                                 "partials); excluded from t_fin like the reference, overlapped with chunk kernels"},
     }
     print(json.dumps(line), flush=True)
 

@@ -176,8 +176,10 @@ typedef enum sp_trace_kind {
   SP_TRACE_MERGE = 6,    /* gpu: merge kernel                              */
   SP_TRACE_ROUTE = 7,    /* host: MoE call entry -> dispatch (x read-back,
                             routing, grouping)                             */
-  SP_TRACE_RETURN = 8    /* host: forward enqueue done -> return to caller
+  SP_TRACE_RETURN = 8,   /* host: forward enqueue done -> return to caller
                             (CC join, tail)                                */
+  SP_TRACE_YCC = 9       /* transfer: CC partial host -> HBM (prefill-size
+                            partials; small ones are read in place)        */
 } sp_trace_kind;
 typedef struct sp_trace_record {
   int32_t index;  /* 1-based item index within its stream                */

@@ -20,7 +20,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_native" / "libsliced.so"
 SP_F32, SP_BF16 = 0, 1
 SP_IO_DEVICE, SP_IO_HOST, SP_NO_CC_THREADS = 0, 1, 2
 ACT_CODES = {"identity": 0, "silu": 1, "gelu": 2}
-TRACE_KINDS = ("launch", "gg", "cg", "cg_prime", "copy", "cc", "merge", "route", "return")
+TRACE_KINDS = ("launch", "gg", "cg", "cg_prime", "copy", "cc", "merge", "route", "return", "ycc")
 STREAM_NAMES = ("launch", "transfer", "gpu", "cpu")
 
 # symbol -> (restype, argtypes); the CPU suite checks this table against include/sliced.h

@@ -1346,12 +1346,18 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     if (ycc_copy) {
       // after ws's allocation and the previous forward's finalize (reads these buffers)
       SP_CUDA(cudaStreamWaitEvent(C->s_aux, C->ev_ws, 0));
+      double ycc_bytes = 0.0;
+      for (int c = 0; c < n_calls; ++c)
+        if (fa.c[c].y_cc == ws[c].ycc) ycc_bytes += double(calls[c].tokens - calls[c].n_g) * N * 4;
+      // the reference's separate Y_cc transfer (pipeline.py:367-383), measured on its own
+      GpuSpan yspan(C, C->s_aux, 1, SP_TRACE_YCC, ycc_bytes);
       for (int c = 0; c < n_calls; ++c) {
         const int64_t Tcc = calls[c].tokens - calls[c].n_g;
         if (fa.c[c].y_cc != ws[c].ycc) continue;
         SP_CUDA(cudaMemcpyAsync(ws[c].ycc, hp + p_ycc[c], size_t(Tcc) * N * 4, cudaMemcpyHostToDevice,
                                 C->s_aux));
       }
+      yspan.end();
       SP_CUDA(cudaEventRecord(C->ev_ycc, C->s_aux));
       SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_ycc, 0));
     }
