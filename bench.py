@@ -114,14 +114,38 @@ def metric_name(args):
 # planning
 
 
+# Host threads the committed profiles were measured with (the 1-GPU pool box:
+# 16 vCPUs, all of them running the CC block).
+PROFILE_HOST_THREADS = 16
+
+
+def rank_host_threads() -> int:
+    return int(os.environ.get("SP_HOST_THREADS", "0") or 0) or (os.cpu_count() or PROFILE_HOST_THREADS)
+
+
 def load_profile(path):
+    """The fitted profile; with fewer host threads per rank than it was measured
+    with (one process per GPU sharing the host), the CPU terms are scaled by
+    the thread ratio -- the CC block runs on this rank's share of the cores."""
     from paper_2411_15715_b200 import costs
     from paper_2411_15715_b200.b200_profile import FALLBACK_DECODE
 
     p = Path(path)
     if p.exists():
-        return costs.load_profile(p), str(p.relative_to(ROOT) if p.is_relative_to(ROOT) else p)
-    return costs.profile_from_dict(FALLBACK_DECODE), "fallback (b200_profile.FALLBACK_DECODE)"
+        prof, src = costs.load_profile(p), str(p.relative_to(ROOT) if p.is_relative_to(ROOT) else p)
+    else:
+        prof, src = costs.profile_from_dict(FALLBACK_DECODE), "fallback (b200_profile.FALLBACK_DECODE)"
+    threads = rank_host_threads()
+    if threads < PROFILE_HOST_THREADS:
+        doc = costs.profile_to_dict(prof)
+        k = PROFILE_HOST_THREADS / threads
+        for g in doc.get("gemm", {}).values():
+            if "cpu" in g:
+                g["cpu"]["alpha"] *= k
+                g["cpu"]["beta"] *= k
+        prof = costs.profile_from_dict(doc)
+        src += f" (CPU terms x{k:g}: {threads} host threads per rank)"
+    return prof, src
 
 
 def sp_precision_fp16():
