@@ -56,6 +56,7 @@ from .planner import (
     lipschitz_bound,
     prompt_speedup,
     solve_ng,
+    solve_ng_layer,
     solve_rates_grid,
     solve_rcg,
 )

@@ -353,6 +353,70 @@ def solve_ng(
     return TokenPlan(n_g=best_ng, t_fin_prompt=best_t, baseline_t_fin=baseline, candidates=tuple(scored))
 
 
+@dataclass(frozen=True)
+class LayerTokenPlan:
+    n_g: tuple[int, ...]       # per expert of the layer
+    link_s: float              # modelled host-link time of the layer
+    cpu_s: float               # modelled host CC time of the layer
+
+
+def solve_ng_layer(
+    profile: HardwareProfile, layer: LayerSpec, tokens: Sequence[int], rates: SlicingRates,
+    chunk_bytes: float = 8 << 20,
+) -> LayerTokenPlan:
+    """EXTENSION (not in the reference): token split of a whole MoE layer.
+
+    ``solve_ng`` (token_assigner.py:104-137, bit-exact above) plans one expert
+    as if it had the host link and the host cores to itself.  The experts of
+    a layer share both, and the runtime streams an expert's CC chunks only
+    when some of its rows run on the GPU (n_g > 0).  Per expert this takes
+    n_g in {T_e (every row on the GPU: CC chunks streamed, host idle),
+    0 (every row on the host: only CG streamed)} and greedily moves experts to
+    the host side while the layer's max(link, host) time drops:
+        link_e = alpha_P * chunks + (cg + cc * [n_g > 0]) * G * W * beta_P
+        cpu_e  = G * (alpha_C + (T_e - n_g) * cc * M * H * beta_C)
+    (G GEMMs per expert = layer.n_gemms, W = layer.weight_bytes).  Ties go to
+    the lower expert index; deterministic."""
+    gemm, pcie = profile.gemm[layer.precision], profile.require_pcie()
+    G = float(layer.n_gemms)
+    W = float(layer.weight_bytes)
+    mh = float(layer.model_dim) * layer.hidden_dim
+    cc, cg = rates.cc, rates.cg
+
+    def link(t: int, ng: int) -> float:
+        nbytes = (cg + (cc if ng > 0 else 0.0)) * G * W
+        return pcie.alpha * math.ceil(nbytes / chunk_bytes) + nbytes * pcie.beta if nbytes > 0 else 0.0
+
+    def cpu(t: int, ng: int) -> float:
+        kept = t - ng
+        return G * (gemm.cpu.alpha + kept * cc * mh * gemm.cpu.beta) if kept > 0 and cc > 0 else 0.0
+
+    ng = [int(t) for t in tokens]  # start: every row on the GPU
+
+    def layer_time(plan):
+        lk = sum(link(t, n) for t, n in zip(tokens, plan))
+        cp = sum(cpu(t, n) for t, n in zip(tokens, plan))
+        return max(lk, cp), lk, cp
+
+    best, _, _ = layer_time(ng)
+    while True:
+        move, move_t = None, best
+        for e, t in enumerate(tokens):
+            if ng[e] == 0 or t == 0:
+                continue
+            trial = list(ng)
+            trial[e] = 0
+            tt, _, _ = layer_time(trial)
+            if tt < move_t:
+                move, move_t = e, tt
+        if move is None:
+            break
+        ng[move] = 0
+        best = move_t
+    _, lk, cp = layer_time(ng)
+    return LayerTokenPlan(n_g=tuple(ng), link_s=lk, cpu_s=cp)
+
+
 def prompt_speedup(
     profile: HardwareProfile, layer: LayerSpec, tokens: int, rates: SlicingRates,
     transfer_model: str = TRANSFER_LITERAL,

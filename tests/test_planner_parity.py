@@ -174,3 +174,28 @@ def test_live_differential_random_profiles(ref):
             assert ga.per_layer_rgg == gb.per_layer_rgg and ga.bytes_used == gb.bytes_used
             assert [(s.layer_index, s.rgg, s.importance) for s in ga.trace] == \
                    [(s.layer_index, s.rgg, s.importance) for s in gb.trace]
+
+
+def test_solve_ng_layer_extension_limits():
+    """planner.solve_ng_layer (extension, no reference counterpart): a free host
+    keeps every expert's rows on the host, a very slow host none; deterministic."""
+    import copy
+
+    from paper_2411_15715_b200 import costs
+
+    base = costs.profile_to_dict(PROFILES[0]) if isinstance(PROFILES, list) else costs.profile_to_dict(
+        next(iter(PROFILES.values())))
+    layer_ = sp.LayerSpec(4096, 14336, n_gemms=3, precision=sp.Precision.FP16)
+    rates = sp.SlicingRates(0.35, 0.15, 0.5)
+    toks = [100, 120, 130, 140]
+    fast, slow = copy.deepcopy(base), copy.deepcopy(base)
+    for doc, k in ((fast, 1e-6), (slow, 1e6)):
+        for g in doc["gemm"].values():
+            g["cpu"]["alpha"] *= k
+            g["cpu"]["beta"] *= k
+    pf = sp.solve_ng_layer(costs.profile_from_dict(fast), layer_, toks, rates)
+    ps = sp.solve_ng_layer(costs.profile_from_dict(slow), layer_, toks, rates)
+    assert pf.n_g == (0, 0, 0, 0)
+    assert ps.n_g == tuple(toks)
+    again = sp.solve_ng_layer(costs.profile_from_dict(fast), layer_, toks, rates)
+    assert again == pf
