@@ -1215,9 +1215,17 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   if (cc_async) cc_submit(C, cc_work);
 
   // ---- GG blocks (HBM resident): the decode-size calls share one grouped launch ----
+  // GG work is off the critical path (the copy stream paces the step), but it
+  // shares the compute stream with the chunk kernels, and a chunk kernel that
+  // waits behind it frees its ring slot late and stalls the copies.  So the GG
+  // work is cut into jobs: the grouped launch goes first (queued behind the
+  // first chunk copy), every other GG block is slotted in after a chunk kernel,
+  // into the compute stream's idle time while the next copy is in flight.
+  std::vector<std::function<int()>> gg_jobs;
   {
     const int tt_max = max_token_tile(M);
     std::vector<int> group;
+    std::vector<int> singles;
     for (int c = 0; c < n_calls; ++c) {
       const sp_layer* L = calls[c].layer;
       const int Te = int(calls[c].tokens);
@@ -1225,16 +1233,8 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       const bool tc = use_tc(L, Te);
       const sp_layer* L0 = group.empty() ? L : calls[group[0]].layer;
       const bool same = L->d.wdtype == L0->d.wdtype && L->d.gated == L0->d.gated && L->d.act == L0->d.act;
-      if (!tc && Te <= tt_max && same && int(group.size()) < kMaxGroup) {
-        group.push_back(c);
-        continue;
-      }
-      BlockView b{static_cast<const char*>(L->gg), L->gg_w3_off, L->gg_w2_off, L->h_gg};
-      // weight bytes streamed: once on the tensor-core path, once per token tile otherwise
-      const double passes = tc ? 1.0 : double((Te + tt_max - 1) / tt_max);
-      GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, double(L->gg_bytes) * passes);
-      SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, 0, Te, C->s_comp));
-      span.end();
+      if (!tc && Te <= tt_max && same && int(group.size()) < kMaxGroup) group.push_back(c);
+      else singles.push_back(c);
     }
     if (!group.empty()) {
       // CTAs proportional to each block's rows, one wave over the SMs
@@ -1263,21 +1263,41 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         ws[c].S += nc;
       }
       const int tt = te_max <= 1 ? 1 : te_max <= 2 ? 2 : 4;
-      // The GG launch is off the critical path (the copy stream paces the step):
-      // it is queued behind the first chunk copy, so the GPU starts it from a
-      // full queue -- no host-enqueue bubble inside its span -- and it still
-      // ends long before the last chunk kernel needs the stream.
-      if (!items.empty()) SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_copied[items[0].slot], 0));
-      GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, bytes);
-      if (C->trace.kslot_cur >= 0)
-        for (int i = 0; i < g.n; ++i) {
-          g.a[i].kspan0 = C->trace.kspan + C->trace.kslot_cur;
-          g.a[i].kspan1 = C->trace.kspan + kKSlots + C->trace.kslot_cur;
-        }
-      SP_TRY(launch_group(C, calls[group[0]].layer, tt, g, cta, C->s_comp));
-      span.end();
+      const sp_layer* L0 = calls[group[0]].layer;
+      gg_jobs.push_back([&, g, cta, tt, bytes, L0]() mutable -> int {
+        // queued behind the first chunk copy: the GPU starts it from a full
+        // queue (no host-enqueue bubble inside its span)
+        if (!items.empty()) SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_copied[items[0].slot], 0));
+        GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, bytes);
+        if (C->trace.kslot_cur >= 0)
+          for (int i = 0; i < g.n; ++i) {
+            g.a[i].kspan0 = C->trace.kspan + C->trace.kslot_cur;
+            g.a[i].kspan1 = C->trace.kspan + kKSlots + C->trace.kslot_cur;
+          }
+        SP_TRY(launch_group(C, L0, tt, g, cta, C->s_comp));
+        span.end();
+        return SP_OK;
+      });
+    }
+    for (int c : singles) {
+      gg_jobs.push_back([&, c, tt_max]() -> int {
+        const sp_layer* L = calls[c].layer;
+        const int Te = int(calls[c].tokens);
+        const bool tc = use_tc(L, Te);
+        BlockView b{static_cast<const char*>(L->gg), L->gg_w3_off, L->gg_w2_off, L->h_gg};
+        // weight bytes streamed: once on the tensor-core path, once per token tile otherwise
+        const double passes = tc ? 1.0 : double((Te + tt_max - 1) / tt_max);
+        GpuSpan span(C, C->s_comp, 2, SP_TRACE_GG, double(L->gg_bytes) * passes);
+        SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, 0, Te, C->s_comp));
+        span.end();
+        return SP_OK;
+      });
     }
   }
+  size_t next_gg = 0;
+  if (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());
+  if (items.empty())
+    while (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());
 
   // ---- chunk kernels, in copy order, each followed by the copy its slot frees ----
   for (size_t i = 0; i < items.size(); ++i) {
@@ -1305,7 +1325,9 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     }
     SP_CUDA(cudaEventRecord(C->ev_free[it.slot], C->s_comp));
     if (next_copy < items.size()) SP_TRY(enqueue_copy());
+    if (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());  // into the wait for the next copy
   }
+  while (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());
 
   const double t_enq_done = now_s();
   host_span(C, 0, SP_TRACE_LAUNCH, t_call, t_enq_done, 0.0);
