@@ -181,16 +181,24 @@ def plan_rates(args, tokens_per_step):
 
     MoE decode is modelled the reference's way, n_gemms = active experts x 3
     (PAPER.md:157), with the expected number of experts a batch activates and
-    the tokens each of them sees (hard part 6)."""
+    the tokens each of them sees (hard part 6).  Under
+    expert parallelism (WORLD_SIZE > 1) every rank routes the global batch and
+    plans for the experts it owns."""
     import math
 
     import paper_2411_15715_b200 as sp
 
     hidden = getattr(args, "shard_hidden", args.hidden_dim)
-    e_act = min(expected_active(args.experts, args.top_k, tokens_per_step), args.experts) if args.experts > 1 \
-        else 1.0
-    n_gemms = max(args.top_k, round(e_act)) * 3
-    t_expert = max(1, math.ceil(tokens_per_step * args.top_k / max(e_act, 1.0)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.experts > 1:
+        # every rank routes the global batch; a rank runs only its own experts
+        t_glob = tokens_per_step * world
+        e_act = min(expected_active(args.experts, args.top_k, t_glob), args.experts)
+        e_loc = args.experts / world * (1.0 - (1.0 - args.top_k / args.experts) ** t_glob)
+        n_gemms = max(1, round(e_loc)) * 3
+        t_expert = max(1, math.ceil(t_glob * args.top_k / max(e_act, 1.0)))
+    else:
+        n_gemms, t_expert = 3, max(1, tokens_per_step)
     profile, source = load_profile(decode_profile_for(args.profile, t_expert))
     layer = sp.LayerSpec(args.model_dim, hidden, n_gemms=n_gemms, precision=sp.Precision.FP16)
     budget = args.budget_frac * layer.layer_bytes
