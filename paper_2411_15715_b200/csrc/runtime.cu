@@ -382,10 +382,6 @@ static int fill_rows(sp_layer* L, const void* w1t, const void* w3t, const void* 
   return SP_OK;
 }
 
-static int pack_layer(sp_layer* L, const void* w1t, const void* w3t, const void* w2) {
-  SP_TRY(place_layer(L));
-  return fill_rows(L, w1t, w3t, w2);
-}
 
 // Row-major [H, M] / [H, N] copies of a placed layer's weights (GG rows read
 // back from HBM): the input of a re-slice.
