@@ -54,6 +54,8 @@ typedef enum sp_act { SP_ACT_IDENTITY = 0, SP_ACT_SILU = 1, SP_ACT_GELU = 2 } sp
 #define SP_IO_DEVICE 0u     /* x / y are device pointers (inputs resident in HBM) */
 #define SP_IO_HOST 1u       /* x / y are host pointers; H2D / D2H inside the call  */
 #define SP_NO_CC_THREADS 2u /* run the CC slice on the calling thread only         */
+#define SP_X_TO_BF16 4u     /* with SP_IO_HOST and f32 x: round x to bf16 while staging
+                               it (the activations of a bf16 layer), no caller-side cast */
 
 typedef struct sp_layer* sp_layer_t;
 

@@ -18,7 +18,7 @@ from .errors import NativeError, raise_for
 LIB_PATH = Path(__file__).resolve().parent / "_native" / "libsliced.so"
 
 SP_F32, SP_BF16 = 0, 1
-SP_IO_DEVICE, SP_IO_HOST, SP_NO_CC_THREADS = 0, 1, 2
+SP_IO_DEVICE, SP_IO_HOST, SP_NO_CC_THREADS, SP_X_TO_BF16 = 0, 1, 2, 4
 ACT_CODES = {"identity": 0, "silu": 1, "gelu": 2}
 TRACE_KINDS = ("launch", "gg", "cg", "cg_prime", "copy", "cc", "merge", "route", "return", "ycc")
 STREAM_NAMES = ("launch", "transfer", "gpu", "cpu")

@@ -962,6 +962,35 @@ static int cc_join_with_tail(Context* C, const std::function<int()>& tail) {
 // ---------------------------------------------------------------------------
 // forward
 
+// fp32 -> bf16 bit patterns, round to nearest even: u + 0x7fff + ((u >> 16) & 1),
+// the same integer arithmetic as the Python fallback (NaNs are not special-cased).
+// Native so host activations never go through a multi-threaded framework cast,
+// whose spinning worker threads steal the cores the CC block runs on.
+__attribute__((target("avx512f,avx512bw"))) static void round_bf16_avx512(const float* src, uint16_t* dst,
+                                                                           int64_t n) {
+  const __m512i bias = _mm512_set1_epi32(0x7fff), one = _mm512_set1_epi32(1);
+  int64_t i = 0;
+  for (; i + 16 <= n; i += 16) {
+    __m512i u = _mm512_castps_si512(_mm512_loadu_ps(src + i));
+    u = _mm512_add_epi32(u, _mm512_add_epi32(bias, _mm512_and_si512(_mm512_srli_epi32(u, 16), one)));
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), _mm512_cvtepi32_epi16(_mm512_srli_epi32(u, 16)));
+  }
+  for (; i < n; ++i) {
+    uint32_t u;
+    memcpy(&u, src + i, 4);
+    dst[i] = uint16_t((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+  }
+}
+
+static void round_bf16_host(const float* src, uint16_t* dst, int64_t n) {
+  if (host_has_avx512()) return round_bf16_avx512(src, dst, n);
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t u;
+    memcpy(&u, src + i, 4);
+    dst[i] = uint16_t((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+  }
+}
+
 static int forward_batch(Context* C, const sp_call* calls, int n_calls, const void* x, int xdtype,
                          int64_t T, void* y, int ydtype, unsigned flags, cudaStream_t user,
                          const void* x_host_ready = nullptr) {
@@ -971,6 +1000,13 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   if (T < 1) return fail(SP_ERR_SHAPE, "input must have at least one row, got T=%lld", (long long)T);
   if ((xdtype != SP_F32 && xdtype != SP_BF16) || (ydtype != SP_F32 && ydtype != SP_BF16))
     return fail(SP_ERR_VALUE, "x/y dtype must be SP_F32 or SP_BF16");
+  // SP_X_TO_BF16: the caller's f32 x is rounded into the bf16 staging copy; every
+  // consumer (GPU upload, CC threads) then sees bf16 activations
+  const bool stage_bf16 = (flags & SP_X_TO_BF16) && xdtype == SP_F32;
+  if ((flags & SP_X_TO_BF16) && !(flags & SP_IO_HOST))
+    return fail(SP_ERR_VALUE, "SP_X_TO_BF16 needs SP_IO_HOST");
+  const void* x_src = x;
+  if (stage_bf16) xdtype = SP_BF16;
   int64_t M = -1, N = -1;
   for (int c = 0; c < n_calls; ++c) {
     const sp_call& k = calls[c];
@@ -1171,11 +1207,14 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   const void* x_dev = x;
   const void* x_host = nullptr;
   if (host_io) {
-    memcpy(hp + p_x, x, size_t(T) * M * xel);
+    if (stage_bf16)
+      round_bf16_host(static_cast<const float*>(x_src), reinterpret_cast<uint16_t*>(hp + p_x), T * M);
+    else
+      memcpy(hp + p_x, x, size_t(T) * M * xel);
     SP_CUDA(cudaMemcpyAsync(dws + o_xdev, hp + p_x, size_t(T) * M * xel, cudaMemcpyHostToDevice,
                             C->s_comp));
     x_dev = dws + o_xdev;
-    x_host = x;
+    x_host = stage_bf16 ? static_cast<const void*>(hp + p_x) : x;
   } else if (need_cc && x_host_ready) {
     x_host = x_host_ready;  // already read back by the caller (sp_moe_forward): no GPU wait
   } else if (need_cc) {
@@ -1502,6 +1541,14 @@ static int moe_forward(Context* C, const sp_layer_t* layers, int E, const float*
   const size_t xel = xdtype == SP_BF16 ? 2 : 4;
   const bool host_io = flags & SP_IO_HOST;
   const double t_route0 = now_s();
+  if ((flags & SP_X_TO_BF16) && host_io && xdtype == SP_F32) {
+    // route on the rounded activations the experts will see
+    SP_TRY(C->xroute.ensure(size_t(T) * M * 2));
+    round_bf16_host(static_cast<const float*>(x), static_cast<uint16_t*>(C->xroute.p), T * M);
+    x = C->xroute.p;
+    xdtype = SP_BF16;
+    flags &= ~SP_X_TO_BF16;
+  }
   // one read of x serves the router and every CC block
   const void* xh = x;
   if (!host_io) {
@@ -1914,37 +1961,9 @@ int sp_cc_forward_host(sp_layer_t L, const void* x, int xdtype, int64_t T, float
   return SP_OK;
 }
 
-// fp32 -> bf16 bit patterns, round to nearest even: u + 0x7fff + ((u >> 16) & 1),
-// the same integer arithmetic as the Python fallback (NaNs are not special-cased).
-// Native so host activations never go through a multi-threaded framework cast,
-// whose spinning worker threads steal the cores the CC block runs on.
-__attribute__((target("avx512f,avx512bw"))) static void round_bf16_avx512(const float* src, uint16_t* dst,
-                                                                           int64_t n) {
-  const __m512i bias = _mm512_set1_epi32(0x7fff), one = _mm512_set1_epi32(1);
-  int64_t i = 0;
-  for (; i + 16 <= n; i += 16) {
-    __m512i u = _mm512_castps_si512(_mm512_loadu_ps(src + i));
-    u = _mm512_add_epi32(u, _mm512_add_epi32(bias, _mm512_and_si512(_mm512_srli_epi32(u, 16), one)));
-    _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), _mm512_cvtepi32_epi16(_mm512_srli_epi32(u, 16)));
-  }
-  for (; i < n; ++i) {
-    uint32_t u;
-    memcpy(&u, src + i, 4);
-    dst[i] = uint16_t((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
-  }
-}
-
 int sp_round_bf16(const float* src, uint16_t* dst, int64_t n) {
   if (n < 0 || (n > 0 && (!src || !dst))) return fail(SP_ERR_VALUE, "NULL argument");
-  if (host_has_avx512()) {
-    round_bf16_avx512(src, dst, n);
-    return SP_OK;
-  }
-  for (int64_t i = 0; i < n; ++i) {
-    uint32_t u;
-    memcpy(&u, src + i, 4);
-    dst[i] = uint16_t((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
-  }
+  round_bf16_host(src, dst, n);
   return SP_OK;
 }
 

@@ -272,6 +272,17 @@ def _host_activations(x, dtype: str) -> tuple[np.ndarray, int]:
     return np.ascontiguousarray(np.asarray(x), dtype=np.float32), nat.SP_F32
 
 
+def _host_input(x, dtype: str) -> tuple[np.ndarray, int, int]:
+    """Host activations for a forward with SP_IO_HOST: (array, xdtype, extra flags).
+    bf16 layers get f32 x plus SP_X_TO_BF16 -- the runtime rounds it while
+    staging, into persistent pinned memory (no caller-side cast / allocation)."""
+    a = np.asarray(x)
+    if dtype == "bf16" and a.dtype != np.uint16:
+        return np.ascontiguousarray(a, dtype=np.float32), nat.SP_F32, nat.SP_X_TO_BF16
+    xh, code = _host_activations(a, dtype)
+    return xh, code, 0
+
+
 @dataclass
 class CallSpec:
     """One layer application inside a batched forward (sp_call)."""
@@ -334,12 +345,12 @@ def forward_calls(calls: Sequence[CallSpec], x, out=None, host_threads_off: bool
     # host I/O
     if torch is not None and isinstance(x, torch.Tensor):
         x = x.detach().float().numpy()
-    xh, xcode = _host_activations(x, calls[0].layer.dtype)
+    xh, xcode, xflag = _host_input(x, calls[0].layer.dtype)
     if xh.ndim != 2 or xh.shape[1] != M:
         raise ShapeMismatch(f"input is {xh.shape} but the layer expects {M} features")
     y = np.empty((xh.shape[0], N), dtype=np.float32) if out is None else out
     nat.check(nat.lib().sp_forward_batch(arr, len(calls), xh.ctypes.data, xcode, xh.shape[0],
-                                         y.ctypes.data, nat.SP_F32, flags | nat.SP_IO_HOST, None))
+                                         y.ctypes.data, nat.SP_F32, flags | xflag | nat.SP_IO_HOST, None))
     return y
 
 
@@ -638,10 +649,10 @@ class MoEDispatch:
             return out
         if torch is not None and isinstance(x, torch.Tensor):
             x = x.detach().float().numpy()
-        xh, xcode = _host_activations(x, self.dtype)
+        xh, xcode, xflag = _host_input(x, self.dtype)
         y = np.empty((xh.shape[0], self.N), dtype=np.float32) if out is None else out
         st = self.fn(self.arr, self.E, self.rp, self.k, xh.ctypes.data, xcode, xh.shape[0], y.ctypes.data,
-                     nat.SP_F32, nat.SP_IO_HOST, None)
+                     nat.SP_F32, nat.SP_IO_HOST | xflag, None)
         if st:
             nat.check(st)
         return y
