@@ -444,6 +444,18 @@ static int max_token_tile(int64_t M) {
   return 0;
 }
 
+// Most hidden rows one ffn_block CTA can own (its phase-1 partials live in
+// shared memory next to the x tile and a 2-stage ring): a grouped launch of many
+// experts must not pack more rows than this into one CTA.
+static int64_t max_rows_per_cta(int64_t M, int gated, int tt, int xel) {
+  const int64_t G = gated ? 2 : 1;
+  const int64_t kt = round_up(M, 256);
+  const int64_t fixed = int64_t(tt) * kt * 4 + (int64_t(tt) * M * xel + 15) / 16 * 16 + (2 * kMaxStages + 1) * 8 + 128;
+  const int64_t per_row = int64_t(kConsumers) * G * tt * 4 + tt * 4;
+  const int64_t room = int64_t(kSmemLimit) - fixed - 2 * int64_t(g_stage_bytes) - 1024;
+  return std::max<int64_t>(1, room / per_row);
+}
+
 template <typename WT, int TT, bool GATED, int NV>
 static int launch_ffn_t(Context* C, const FfnGroup& grp, int grid, cudaStream_t s) {
   constexpr int G = GATED ? 2 : 1;
@@ -1288,6 +1300,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         const int Te = int(calls[c].tokens);
         int nc = int(double(C->num_sms) * double(L->h_gg) / double(rows_total));
         nc = std::max(1, std::min(nc, block_grid(C, L->h_gg)));
+        // many experts in one group: more CTAs than SMs rather than too many rows per CTA
+        const int64_t cap = max_rows_per_cta(M, L->d.gated, te_max <= 1 ? 1 : te_max <= 2 ? 2 : 4,
+                                             xdtype == SP_BF16 ? 2 : 4);
+        nc = std::min(std::max<int>(nc, int((L->h_gg + cap - 1) / cap)), block_grid(C, L->h_gg));
         BlockView b{static_cast<const char*>(L->gg), L->gg_w3_off, L->gg_w2_off, L->h_gg};
         FfnArgs a = ffn_args(C, L, b, x_dev, xdtype, M, ws[c], Te);
         set_tokens(a, calls[c].token_ids, Te, 0, Te);

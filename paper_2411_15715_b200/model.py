@@ -30,7 +30,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .schedule import SlicingRates
-from .sliced import MoEDispatch, SlicedFFN
+from .sliced import CallSpec, MoEDispatch, SlicedFFN, forward_calls, moe_route
 
 
 @dataclass
@@ -139,6 +139,49 @@ class SlicedMixtral:
 
     def _moe(self, d: int, h, out=None):
         return self.dispatch[d](h, out)
+
+    # -- prefill -----------------------------------------------------------------
+    def prefill(self, x, token_planner=None):
+        """The prompt x [P, M] through every layer: causal attention over the
+        prompt (K / V written to cache positions [0, P)), then the sliced MoE
+        with the prompt-phase token split -- ``token_planner(T_e) -> n_g`` per
+        expert (e.g. the reference's solve_ng; None keeps every row on the
+        host for the CC columns).  Routing uses the runtime's router, as decode
+        does.  Returns the hidden states [P, M]."""
+        torch = self.torch
+        cfg, hd = self.cfg, self.head_dim
+        P = x.shape[0]
+        cos, sin = self.cos[:P][:, None, :], self.sin[:P][:, None, :]
+
+        def rope(t):  # [P, heads, hd]
+            tf = t.float().view(*t.shape[:-1], -1, 2)
+            a, b = tf[..., 0], tf[..., 1]
+            return torch.stack((a * cos - b * sin, a * sin + b * cos), -1).flatten(-2).to(t.dtype)
+
+        for l in range(cfg.layers):
+            h = self._rms(x, self.attn[l]["n1"])
+            qkv = h @ self.attn[l]["wqkv"].t()
+            q = rope(qkv[:, : cfg.heads * hd].view(P, cfg.heads, hd))
+            k = rope(qkv[:, cfg.heads * hd: (cfg.heads + cfg.kv_heads) * hd].view(P, cfg.kv_heads, hd))
+            v = qkv[:, (cfg.heads + cfg.kv_heads) * hd:].view(P, cfg.kv_heads, hd)
+            self.kv[l, 0, 0, :, :P] = k.transpose(0, 1)
+            self.kv[l, 1, 0, :, :P] = v.transpose(0, 1)
+            o = torch.nn.functional.scaled_dot_product_attention(
+                q.transpose(0, 1)[None], k.transpose(0, 1)[None], v.transpose(0, 1)[None], is_causal=True,
+                enable_gqa=True)
+            x = x + o[0].transpose(0, 1).reshape(P, cfg.heads * hd) @ self.attn[l]["wo"].t()
+            h2 = self._rms(x, self.attn[l]["n2"])
+            d = l % cfg.distinct
+            ids, gates = moe_route(h2.float().cpu().numpy(), self.routers[d], cfg.top_k)
+            calls = []
+            for e, ffn in enumerate(self.moe_sets[d]):
+                rows, slots = np.nonzero(ids == e)
+                if rows.size:
+                    ng = int(token_planner(rows.size)) if token_planner else 0
+                    calls.append(CallSpec(ffn.layer, rows.astype(np.int32), gates[rows, slots].astype(np.float32),
+                                          min(ng, rows.size)))
+            x = x + forward_calls(calls, h2)
+        return x
 
     # -- CUDA-graph decode ------------------------------------------------------
     # Per layer the torch part (residual add of the previous MoE output, RMSNorm,

@@ -239,3 +239,31 @@ def test_back_to_back_device_forwards(sp, torch, T):
     for x, y in zip(xs, ys):
         ref = orc.dense_forward(q(x.float().cpu().numpy()), q(w1t.T), q(w2t.T), "silu", q(w3t.T))
         assert orc.max_rel_error(y.float().cpu().numpy(), ref) <= BF16_TOL
+
+
+def test_grouped_gg_launch_with_many_experts(sp, torch):
+    """Eight experts with 3 tokens each in one grouped GG launch (a short prompt
+    or a big decode batch), 4608 GG rows each: 8 x 4608 / 148 SMs would put 249
+    rows in a CTA, more than its shared memory holds at a 4-token tile -- the
+    group must spread them over more CTAs.  Reference: torch fp32 on the GPU."""
+    from paper_2411_15715_b200.sliced import CallSpec, SlicedFFN, forward_calls
+
+    E, M, H, T = 8, 4096, 4608, 16
+    g = torch.Generator(device="cuda").manual_seed(55)
+    ws = [tuple((torch.randn(*s, device="cuda", generator=g) / 32).to(torch.bfloat16) for s in ((H, M), (H, M), (M, H)))
+          for _ in range(E)]
+    experts = [SlicedFFN(w1t.cpu(), w2t.cpu(), sp.SlicingRates(0.0, 0.0, 1.0), w3t=w3t.cpu(), dtype="bf16")
+               for w1t, w3t, w2t in ws]
+    x = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16)
+    ids = [torch.tensor([(2 * i) % T, (2 * i + 1) % T, (2 * i + 5) % T], dtype=torch.int32) for i in range(E)]
+    y = forward_calls([CallSpec(e.layer, i.numpy()) for e, i in zip(experts, ids)], x).float()
+    ref = torch.zeros(T, M, device="cuda")
+    xf = x.float()
+    for (w1t, w3t, w2t), i in zip(ws, ids):
+        xi = xf[i.long().cuda()]
+        h = torch.nn.functional.silu(xi @ w1t.float().t()) * (xi @ w3t.float().t())
+        ref.index_add_(0, i.long().cuda(), h @ w2t.float().t())
+    err = ((y - ref).abs().max() / ref.abs().max()).item()
+    assert err <= BF16_TOL, err
+    for e in experts:
+        e.layer.release()

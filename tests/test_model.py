@@ -81,3 +81,30 @@ def test_graph_decode_matches_eager():
         assert err <= 2e-2, (pos, err)
     assert int(m.pos_dev.item()) == 5
     m.release()
+
+
+def test_prefill_then_decode_matches_incremental_decode():
+    """Causal prefill of a short prompt == feeding it token by token through
+    decode_step (same cache contents, same last hidden state)."""
+    import torch
+
+    from paper_2411_15715_b200 import _native as nat
+    from paper_2411_15715_b200.model import DecoderConfig, SlicedMixtral
+    from paper_2411_15715_b200.schedule import SlicingRates
+
+    nat.init(0)
+    cfg = DecoderConfig(layers=2, distinct=2, model_dim=256, hidden_dim=640, experts=4, top_k=2, heads=4,
+                        kv_heads=2, max_seq=16)
+    m = SlicedMixtral(cfg, SlicingRates(0.25, 0.25, 0.5))
+    P = 5
+    xs = (torch.randn(P, 256, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3)) * 0.5).to(
+        torch.bfloat16)
+    inc = [m.decode_step(xs[i:i + 1], i) for i in range(P)]
+    kv_inc = m.kv.clone()
+    m.kv.zero_()
+    pre = m.prefill(xs, token_planner=lambda t: t // 2)
+    err = orc.max_rel_error(pre[-1:].float().cpu().numpy(), inc[-1].float().cpu().numpy())
+    assert err <= 3e-2, err
+    kerr = orc.max_rel_error(m.kv[:, :, :, :, :P].float().cpu().numpy(), kv_inc[:, :, :, :, :P].float().cpu().numpy())
+    assert kerr <= 3e-2, kerr
+    m.release()
