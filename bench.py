@@ -334,9 +334,14 @@ def run_reference(args):
     if rank != 0:
         return
     rates, _, _, _ = plan_rates(args, args.batch)
-    for _ in range(args.warmup):
-        cpu_reference_sample(args, rates, 1, warmup=0)
-    tps, dt, desc, threads = cpu_reference_sample(args, rates, args.steps, warmup=0)
+    # every host thread for the reference's BLAS, also under torchrun (which
+    # exports OMP_NUM_THREADS=1 to each rank)
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=os.cpu_count(), user_api="blas"):
+        for _ in range(args.warmup):
+            cpu_reference_sample(args, rates, 1, warmup=0)
+        tps, dt, desc, threads = cpu_reference_sample(args, rates, args.steps, warmup=0)
     line = {
         "impl": "reference", "metric": metric_name(args), "value": tps, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
@@ -374,6 +379,11 @@ def run_ours(args):
     from paper_2411_15715_b200.expert_parallel import ExpertParallelMoE, local_experts
 
     world, rank, local = dist_env()
+    # SP_BENCH_ONE_GPU=1 (test plumbing): every rank on cuda:0 with gloo, so the
+    # multi-rank bench path runs on a one-GPU box; production is one GPU per rank, NCCL
+    one_gpu = os.environ.get("SP_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     dist = None
@@ -381,7 +391,10 @@ def run_ours(args):
         import torch.distributed as dist
 
         os.environ.setdefault("SP_HOST_THREADS", str(max(1, (os.cpu_count() or 16) // world)))
-        dist.init_process_group("nccl", device_id=device)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
     nat.init(local)
 
     B = args.batch
