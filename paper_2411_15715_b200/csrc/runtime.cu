@@ -640,8 +640,12 @@ static int launch_gemm_t(Context* C, const CUtensorMap& a0, const CUtensorMap& a
     attr_set = true;
   }
   const int ctas = g.m_tiles * g.t_tiles * g.ks;
-  // one CTA per SM with a deep ring, or two per SM with a shallow one
-  const int budget = ctas <= C->num_sms ? kSmemLimit : kSmemLimit / 2 - 1024;
+  // one CTA per SM with a deep ring, or two per SM with a shallow one -- the
+  // latter only when two CTAs with >= 2 stages each actually fit (a 64 KB stage
+  // does not: halving the budget then just left one CTA per SM on 2 stages,
+  // 132 KB instead of 198 KB of loads in flight -- the T = 512 up GEMM)
+  const bool two_per_sm = ctas > C->num_sms && 2 * (2 * STAGE + 1024 + 256) <= kSmemLimit;
+  const int budget = two_per_sm ? kSmemLimit / 2 - 1024 : kSmemLimit;
   g.stages = std::max(2, std::min(6, (budget - 1024 - 256) / STAGE));
   const size_t smem = size_t(g.stages) * STAGE + 1024 + 256;
   if (g.ks > 1) {
