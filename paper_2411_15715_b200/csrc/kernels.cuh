@@ -579,9 +579,51 @@ __global__ void __launch_bounds__(kFinLanes * kFinGroups) finalize_kernel(FinalA
 // token, the slices summed sequentially in slice order -- every thread busy and
 // every load a coalesced float4 (the slice-group layout above would leave 31 of
 // its 32 groups idle).
-__global__ void __launch_bounds__(256) finalize_rows_kernel(FinalArgs p) {
+// Sum each call's S partial slices into its slice 0 (grid.y = call).  Enqueued
+// on the device stream right after a call's last GPU block, so the many-slice
+// reduction of a decode step (one slice per GG-group CTA, per CG chunk CTA)
+// runs while the host CC block is still busy; the finalize that waits for the
+// CC partial then reads one slice per call.  Slices summed in kFinGroups
+// strided groups, groups in order: deterministic.
+__global__ void __launch_bounds__(kFinLanes * kFinGroups) reduce_slices_kernel(FinalArgs p) {
+  __shared__ float4 red[kFinGroups][kFinLanes];
+  const FinalCall& fc = p.c[blockIdx.y];
+  const int64_t count = int64_t(fc.T_e) * p.N;  // floats per slice
+  if (fc.S <= 1 || int64_t(blockIdx.x) * kFinLanes * 4 >= count) return;
+  const int lane = threadIdx.x % kFinLanes, grp = threadIdx.x / kFinLanes;
+  const int64_t col = (int64_t(blockIdx.x) * kFinLanes + lane) * 4;
+  const bool live = col < count;  // N % 4 == 0 on this path
+  float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+  if (live) {
+    int s = grp;
+    for (; s + kFinGroups < fc.S; s += 2 * kFinGroups) {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(fc.part + int64_t(s) * count + col));
+      const float4 b = __ldcg(reinterpret_cast<const float4*>(fc.part + int64_t(s + kFinGroups) * count + col));
+      v0.x += a.x; v0.y += a.y; v0.z += a.z; v0.w += a.w;
+      v1.x += b.x; v1.y += b.y; v1.z += b.z; v1.w += b.w;
+    }
+    for (; s < fc.S; s += kFinGroups) {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(fc.part + int64_t(s) * count + col));
+      v0.x += a.x; v0.y += a.y; v0.z += a.z; v0.w += a.w;
+    }
+  }
+  red[grp][lane] = make_float4(v0.x + v1.x, v0.y + v1.y, v0.z + v1.z, v0.w + v1.w);
+  __syncthreads();
+  if (grp == 0 && live) {
+    float4 tot = red[0][lane];
+#pragma unroll 8
+    for (int g = 1; g < kFinGroups; ++g) {
+      const float4 r = red[g][lane];
+      tot.x += r.x; tot.y += r.y; tot.z += r.z; tot.w += r.w;
+    }
+    *reinterpret_cast<float4*>(const_cast<float*>(fc.part) + col) = tot;  // the workspace is writable
+  }
+}
+
+constexpr int kFinRowsThreads = 128;
+__global__ void __launch_bounds__(kFinRowsThreads) finalize_rows_kernel(FinalArgs p) {
   const int t = blockIdx.y;
-  const int n = (blockIdx.x * 256 + threadIdx.x) * 4;
+  const int n = (blockIdx.x * kFinRowsThreads + threadIdx.x) * 4;
   if (n >= p.N) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int e = p.entry_start[t]; e < p.entry_start[t + 1]; ++e) {
@@ -589,13 +631,27 @@ __global__ void __launch_bounds__(256) finalize_rows_kernel(FinalArgs p) {
     const int i = p.entry_row[e];
     const int64_t stride = int64_t(fc.T_e) * p.N;
     const float* base = fc.part + int64_t(i) * p.N + n;
+    // the CC partial may sit in mapped host memory: issue its load first
+    const bool cc = fc.y_cc && i < fc.n_cc;
+    const float4 c = cc ? *reinterpret_cast<const float4*>(fc.y_cc + int64_t(i) * p.N + n)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
     float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < fc.S; ++s) {
+    // 8 slice loads in flight per thread, summed in slice order
+    int s = 0;
+    for (; s + 8 <= fc.S; s += 8) {
+      float4 a[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = __ldcg(reinterpret_cast<const float4*>(base + int64_t(s + j) * stride));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        tot.x += a[j].x; tot.y += a[j].y; tot.z += a[j].z; tot.w += a[j].w;
+      }
+    }
+    for (; s < fc.S; ++s) {
       const float4 a = __ldcg(reinterpret_cast<const float4*>(base + int64_t(s) * stride));
       tot.x += a.x; tot.y += a.y; tot.z += a.z; tot.w += a.w;
     }
-    if (fc.y_cc && i < fc.n_cc) {
-      const float4 c = *reinterpret_cast<const float4*>(fc.y_cc + int64_t(i) * p.N + n);
+    if (cc) {
       tot.x += c.x; tot.y += c.y; tot.z += c.z; tot.w += c.w;
     }
     const float gate = p.entry_gate[e];

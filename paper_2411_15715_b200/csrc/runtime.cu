@@ -560,6 +560,7 @@ static int preload_kernels() {
   SP_TRY((preload_gemm<2, true>()));
   SP_TRY(preload(finalize_kernel, false));
   SP_TRY(preload(finalize_rows_kernel, false));
+  SP_TRY(preload(reduce_slices_kernel, false));
   SP_TRY(preload(finalize_scalar_kernel, false));
   SP_TRY(preload(tc::swiglu_reduce_kernel, false));
   return preload(tc::gather_rows_bf16_kernel, false);
@@ -595,6 +596,8 @@ static bool use_tc(const sp_layer* L, int64_t T) {
   if (L->d.wdtype != SP_BF16) return false;
   return g_tc_min_tokens_env > 0 ? T >= g_tc_min_tokens_env : T > max_token_tile(L->d.model_dim);
 }
+// SP_PREREDUCE=0: leave every partial slice to the finalize (no early reduction)
+static const bool g_prereduce = env_int("SP_PREREDUCE", 1) != 0;
 constexpr int kTcMaxSplits = 24;
 // finalize: per-token rows kernel up to this many slices per call, slice groups beyond
 constexpr int kFinRowsMaxSlices = 16;  // split-K output slices a resident tc block may use
@@ -1405,8 +1408,6 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     fa.entry_gate = reinterpret_cast<const float*>(fa.entry_row + total_rows);
   }
   bool ycc_copy = false;
-  int max_slices = 0;
-  for (int c = 0; c < n_calls; ++c) max_slices = std::max(max_slices, ws[c].S);
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int64_t Tcc = calls[c].tokens - calls[c].n_g;
@@ -1416,6 +1417,22 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     const float* ycc = !has_cc ? nullptr : zc ? reinterpret_cast<const float*>(hp + p_ycc[c]) : ws[c].ycc;
     fa.c[c] = FinalCall{ws[c].part, ws[c].S, ycc, int(Tcc), int(calls[c].tokens)};
   }
+  // The finalize waits for the host CC block: reduce the device partial slices
+  // now, behind the call's last GPU block, so only the CC partial is left for it.
+  if (need_cc && cc_async && g_prereduce && N % 4 == 0) {
+    int64_t most = 0;
+    for (int c = 0; c < n_calls; ++c)
+      if (fa.c[c].S > 1) most = std::max<int64_t>(most, calls[c].tokens * N);
+    if (most > 0) {
+      dim3 grid(unsigned((most / 4 + kFinLanes - 1) / kFinLanes), unsigned(n_calls));
+      reduce_slices_kernel<<<grid, kFinLanes * kFinGroups, 0, C->s_comp>>>(fa);
+      SP_CUDA(cudaGetLastError());
+      ++C->launches;
+      for (int c = 0; c < n_calls; ++c) fa.c[c].S = std::min(fa.c[c].S, 1);
+    }
+  }
+  int max_slices = 0;
+  for (int c = 0; c < n_calls; ++c) max_slices = std::max(max_slices, fa.c[c].S);
   // The tail runs on whichever thread finishes last: this one (GPU work all
   // enqueued) or the CC coordinator (CC block done) -- so finalize is enqueued
   // the moment both are ready, without a thread wake-up in between.
@@ -1440,8 +1457,8 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     }
     GpuSpan span(C, C->s_comp, 2, SP_TRACE_MERGE, 0.0);
     if (N % 4 == 0 && reinterpret_cast<uintptr_t>(fa.out) % 16 == 0 && max_slices <= kFinRowsMaxSlices) {
-      dim3 grid(unsigned((N / 4 + 255) / 256), unsigned(T));
-      finalize_rows_kernel<<<grid, 256, 0, C->s_comp>>>(fa);
+      dim3 grid(unsigned((N / 4 + kFinRowsThreads - 1) / kFinRowsThreads), unsigned(T));
+      finalize_rows_kernel<<<grid, kFinRowsThreads, 0, C->s_comp>>>(fa);
     } else if (N % 4 == 0 && reinterpret_cast<uintptr_t>(fa.out) % 16 == 0) {
       dim3 grid(unsigned((N + 4 * kFinLanes - 1) / (4 * kFinLanes)), unsigned(T));
       finalize_kernel<<<grid, kFinLanes * kFinGroups, 0, C->s_comp>>>(fa);
