@@ -598,6 +598,9 @@ static bool use_tc(const sp_layer* L, int64_t T) {
 }
 // SP_PREREDUCE=0: leave every partial slice to the finalize (no early reduction)
 static const bool g_prereduce = env_int("SP_PREREDUCE", 1) != 0;
+// SP_HOST_MERGE=0: host-output steps finalize on the GPU like device-output ones
+static const bool g_host_merge = env_int("SP_HOST_MERGE", 1) != 0;
+constexpr int64_t kHostMergeMaxElems = int64_t(1) << 16;  // output-row entries x N merged on the host
 constexpr int kTcMaxSplits = 24;
 // finalize: per-token rows kernel up to this many slices per call, slice groups beyond
 constexpr int kFinRowsMaxSlices = 16;  // split-K output slices a resident tc block may use
@@ -1127,7 +1130,18 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   const size_t p_x = palloc(size_t(T) * M * xel);
   std::vector<size_t> p_ycc(n_calls);
   for (int c = 0; c < n_calls; ++c) p_ycc[c] = palloc(size_t(calls[c].tokens) * N * 4);
-  const size_t p_y = palloc(host_io ? size_t(T) * N * yel : 0);
+  // Host output of a small step whose finalize would wait for the host CC block:
+  // the device partials (pre-reduced, read back while the CC block runs) and the
+  // CC partial are merged by the thread that finishes the CC block -- no GPU
+  // launch, kernel and read-back after it.
+  bool any_cc = false;
+  for (int c = 0; c < n_calls; ++c) any_cc |= calls[c].layer->d.b1 > 0 && calls[c].tokens - calls[c].n_g > 0;
+  const bool host_merge = host_io && any_cc && !(flags & SP_NO_CC_THREADS) && g_prereduce && g_host_merge &&
+                          N % 4 == 0 && total_rows * N <= kHostMergeMaxElems;
+  std::vector<size_t> p_dev(n_calls, 0);
+  if (host_merge)
+    for (int c = 0; c < n_calls; ++c) p_dev[c] = palloc(size_t(calls[c].tokens) * N * 4);
+  const size_t p_y = palloc(host_io && !host_merge ? size_t(T) * N * yel : 0);
   const int hb = C->hpin_turn;
   C->hpin_turn ^= 1;
   if (C->hpin_used[hb]) SP_CUDA(cudaEventSynchronize(C->hpin_done[hb]));
@@ -1433,10 +1447,43 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   }
   int max_slices = 0;
   for (int c = 0; c < n_calls; ++c) max_slices = std::max(max_slices, fa.c[c].S);
+  if (host_merge) {
+    for (int c = 0; c < n_calls; ++c)
+      if (calls[c].tokens > 0 && fa.c[c].S > 0)
+        SP_CUDA(cudaMemcpyAsync(hp + p_dev[c], ws[c].part, size_t(calls[c].tokens) * N * 4, cudaMemcpyDeviceToHost,
+                                C->s_comp));
+    SP_CUDA(cudaEventRecord(C->hpin_done[hb], C->s_comp));
+  }
   // The tail runs on whichever thread finishes last: this one (GPU work all
   // enqueued) or the CC coordinator (CC block done) -- so finalize is enqueued
   // the moment both are ready, without a thread wake-up in between.
+  auto host_tail = [=]() -> int {
+    const cudaError_t e = cudaEventSynchronize(C->hpin_done[hb]);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "device partial read-back: %s", cudaGetErrorString(e));
+    const double t0 = now_s();
+    const int32_t* cs = reinterpret_cast<const int32_t*>(hp + p_csr);
+    const int32_t* ccall = cs + (T + 1);
+    const int32_t* crow = ccall + total_rows;
+    const float* cgate = reinterpret_cast<const float*>(crow + total_rows);
+    std::vector<float> rowbuf(ydtype == SP_F32 ? 0 : size_t(N));
+    for (int64_t t = 0; t < T; ++t) {
+      float* acc = ydtype == SP_F32 ? static_cast<float*>(y) + t * N : rowbuf.data();
+      std::fill(acc, acc + N, 0.f);
+      for (int e = cs[t]; e < cs[t + 1]; ++e) {
+        const int c = ccall[e], i = crow[e];
+        const float g = cgate[e];
+        const float* dev = fa.c[c].S > 0 ? reinterpret_cast<const float*>(hp + p_dev[c]) + int64_t(i) * N : nullptr;
+        const float* cc = fa.c[c].y_cc && i < fa.c[c].n_cc ? reinterpret_cast<const float*>(hp + p_ycc[c]) + int64_t(i) * N
+                                                           : nullptr;
+        for (int64_t n = 0; n < N; ++n) acc[n] += g * ((dev ? dev[n] : 0.f) + (cc ? cc[n] : 0.f));
+      }
+      if (ydtype != SP_F32) round_bf16_host(acc, static_cast<uint16_t*>(y) + t * N, N);
+    }
+    host_span(C, 3, SP_TRACE_MERGE, t0, now_s(), 0.0);
+    return SP_OK;
+  };
   auto tail = [=]() -> int {
+    if (host_merge) return host_tail();
     if (ycc_copy) {
       // after ws's allocation and the previous forward's finalize (reads these buffers)
       SP_CUDA(cudaStreamWaitEvent(C->s_aux, C->ev_ws, 0));
@@ -1483,7 +1530,9 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     if (need_cc) SP_TRY(cc_work());
     SP_TRY(tail());
   }
-  if (host_io) {
+  if (host_merge) {
+    // y written by the tail
+  } else if (host_io) {
     SP_CUDA(cudaStreamSynchronize(C->s_comp));
     memcpy(y, hp + p_y, size_t(T) * N * yel);
   } else {
