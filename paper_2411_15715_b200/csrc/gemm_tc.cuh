@@ -68,6 +68,7 @@ struct GemmArgs {
   // split-K partials [tile][ks][NA][128][NT] fp32 and tickets [tile]
   float* partial;
   int* tickets;
+  int dbg_no_mma;  // probe: stream the operands but issue no MMA (SP_TC_DBG_NOMMA)
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) {
         const unsigned char* st = smem + size_t(s) * STAGE;
 #pragma unroll
-        for (int kk = 0; kk < BK / UK; ++kk) {
+        for (int kk = 0; kk < (g.dbg_no_mma ? 0 : BK / UK); ++kk) {
           const uint64_t b = umma_desc(st + NA * A_BYTES + kk * 32, 16, 1024);
 #pragma unroll
           for (int a = 0; a < NA; ++a) {
@@ -394,6 +395,193 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
+  }
+}
+
+// ---- up GEMM on CTA pairs (tcgen05 cta_group::2) ------------------------------
+//
+// The up GEMM is operand-delivery bound: with the MMAs switched off it runs as
+// long as with them (T = 512: 167 vs 152 us), each SM taking in ~55 GB/s of
+// weight + x tiles.  A CTA pair (cluster of 2 on one TPC) issues one
+// M = 256 MMA: rank r holds weight rows m0 + 128 r (its own TMEM accumulators)
+// and HALF of the x tile (tokens t0 + r * NT/2); the tensor cores read the
+// peer's half over the pair.  Per k-block each SM then loads 32 KB of W1/W3
+// and NT/2 token rows instead of NT: 48 KB instead of 64 at NT = 256.
+// Rank 0 issues the MMAs; both ranks' TMA loads complete on rank 0's full
+// barrier (cta_group::2 form), the MMA commits arrive on both ranks' empty
+// barriers and accumulator barrier (multicast), and each rank runs its own
+// epilogue over its 128 rows exactly as gemm_kernel does.
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` (own smem) in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to_rank(const void* p, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+// grid: 2 * pairs * ks CTAs, cluster (2, 1, 1); pair p -> (tile pair, split) like gemm_kernel
+template <int NT, int NA>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_up_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
+                        const __grid_constant__ CUtensorMap tmB, const GemmArgs g) {
+  constexpr int HALF = NT / 2;          // token rows of x this rank loads
+  constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+  constexpr int B_BYTES = HALF * BK * 2;
+  constexpr int STAGE = NA * A_BYTES + B_BYTES;
+  constexpr int TMEM_COLS = (NA * NT) <= 32 ? 32 : (NA * NT) <= 64 ? 64 : (NA * NT) <= 128 ? 128
+                            : (NA * NT) <= 256 ? 256 : 512;
+  static_assert(HALF % 8 == 0, "x half-tile must be whole 8-row swizzle atoms");
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = g.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(S) * STAGE);
+  uint64_t* empty = full + S;
+  uint64_t* tmem_full = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int ks_id = pair % g.ks;
+  const int tp = pair / g.ks;  // = mt_pair * t_tiles + tt
+  const int mt = tp / g.t_tiles, tt = tp % g.t_tiles;
+  const int m0 = (mt * 2 + int(rank)) * BM, t0 = tt * NT;
+  const int nkb = (g.k + BK - 1) / BK;
+  const int kb0 = nkb * ks_id / g.ks, kb1 = nkb * (ks_id + 1) / g.ks;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA0)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // both ranks' barriers initialised before any TMA signals rank 0
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both ranks) ----------------
+    if (lane == 0) {
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int i = kb - kb0, s = i % S;
+        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+        unsigned char* st = smem + size_t(s) * STAGE;
+        const uint32_t lbar = map_to_rank(&full[s], 0);
+        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE);
+        tma_load_2d_pair(st, &tmA0, lbar, kb * BK, m0);
+        if constexpr (NA == 2) tma_load_2d_pair(st + A_BYTES, &tmA1, lbar, kb * BK, m0);
+        tma_load_2d_pair(st + NA * A_BYTES, &tmB, lbar, kb * BK, t0 + int(rank) * HALF);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (rank 0 only) ----------------
+    if (rank == 0) {
+      const uint32_t idesc = umma_idesc(2 * BM, NT, false);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int i = kb - kb0, s = i % S;
+        mbar_wait(&full[s], (i / S) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const unsigned char* st = smem + size_t(s) * STAGE;
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            const uint64_t b = umma_desc(st + NA * A_BYTES + kk * 32, 16, 1024);
+#pragma unroll
+            for (int a = 0; a < NA; ++a)
+              umma_bf16_pair(tmem + uint32_t(a * NT), umma_desc(st + a * A_BYTES + kk * 32, 16, 1024), b, idesc,
+                             (i > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit_pair(&empty[s]);
+          if (kb == kb1 - 1) umma_commit_pair(tmem_full);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5, this rank's 128 rows ----------------
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int m = m0 + row;
+    const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16);
+    if (kb1 > kb0) {
+      mbar_wait(tmem_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+#pragma unroll 1
+    for (int c = 0; c < NT; c += 16) {
+      uint32_t r[NA][16];
+#pragma unroll
+      for (int a = 0; a < NA; ++a) {
+        if (kb1 > kb0) {
+          tmem_ld16(lane_addr + uint32_t(a * NT + c), r[a]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) r[a][e] = 0u;
+        }
+      }
+      if (m >= g.rows) continue;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int t = t0 + c + e;
+        if (t >= g.T) break;
+        if (g.ks > 1) {
+#pragma unroll
+          for (int a = 0; a < NA; ++a)
+            g.z[((int64_t(ks_id) * NA + a) * g.T + t) * g.zld + m] = __uint_as_float(r[a][e]);
+        } else {
+          float v = act_fn(g.act, __uint_as_float(r[0][e]));
+          if constexpr (NA == 2) v *= __uint_as_float(r[1][e]);
+          g.a_out[int64_t(t) * g.lda + m] = __float2bfloat16_rn(v);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // the peer's MMAs / barrier traffic are over before either rank frees or exits
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
   }
 }
 

@@ -184,7 +184,7 @@ def test_full_size_mixtral_expert_bf16(sp, torch):
 
 
 @pytest.mark.parametrize("gated", [True, False])
-@pytest.mark.parametrize("T", [16, 64, 200])
+@pytest.mark.parametrize("T", [16, 64, 200, 300])
 def test_prefill_tensor_core_path(sp, torch, gated, T):
     """T >= 16 bf16 tokens go through the tcgen05 GEMM pair (up + fused SwiGLU,
     down accumulate); CG chunks, the n_g diverted rows and the CC host rows
@@ -202,6 +202,28 @@ def test_prefill_tensor_core_path(sp, torch, gated, T):
         y = ffn(x, n_g=ng).float().cpu().numpy()
         ref = orc.dense_forward(q(x.float().cpu().numpy()), q(w1t.T), q(w2t.T), "silu", q(w3t.T) if gated else None)
         assert orc.max_rel_error(y, ref) <= BF16_TOL, (cc, cg, ng)
+
+
+@pytest.mark.parametrize("M,H,T", [(1024, 3000, 300), (768, 1100, 256), (4096, 14336, 512)])
+def test_prefill_cta_pair_up_gemm(sp, torch, M, H, T):
+    """256-token tiles run the up GEMM on CTA pairs (gemm_up_pair_kernel:
+    tcgen05 cta_group::2, M = 256 across two SMs, each loading half the x
+    tile): split-K z partials (resident, few tiles), an odd row-tile count
+    (the last pair's second CTA is past the rows), and a whole Mixtral expert
+    at T = 512 with the direct SwiGLU epilogue."""
+    from paper_2411_15715_b200.sliced import SlicedFFN
+
+    rng = np.random.default_rng(M + H + T)
+    w1t, w3t, w2t = (rng.standard_normal(s).astype(np.float32) / 16 for s in ((H, M), (H, M), (M, H)))
+    ffn = SlicedFFN(w1t, w2t, sp.SlicingRates(0.0, 0.0, 1.0), w3t=w3t, activation="silu", dtype="bf16")
+    x = torch.from_numpy(rng.standard_normal((T, M)).astype(np.float32)).cuda().to(torch.bfloat16)
+    y0 = ffn(x)
+    assert torch.equal(y0, ffn(x))
+    q = orc.bf16_round
+    rows = slice(None) if T <= 300 else slice(0, T, 7)  # fp64 oracle on a token subset at full size
+    xs = q(x.float().cpu().numpy())[rows]
+    ref = orc.dense_forward(xs, q(w1t.T), q(w2t.T), "silu", q(w3t.T))
+    assert orc.max_rel_error(y0.float().cpu().numpy()[rows], ref) <= BF16_TOL
 
 
 def test_prefill_moe_tensor_core_path(sp, torch):
