@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=1, help="decode tokens per step per GPU")
     ap.add_argument("--budget-frac", type=float, default=0.5,
                     help="GPU budget as a fraction of each expert's bytes (planner units)")
+    ap.add_argument("--force-cc", type=float, default=-1.0,
+                    help="probe only: override the planner's r_CC (r_CG = 1 - r_GG - r_CC); the line says so")
     ap.add_argument("--experts", type=int, default=8)
     ap.add_argument("--top-k", type=int, default=2)
     ap.add_argument("--profile", default=str(ROOT / "profiles" / "b200_decode.json"))
@@ -206,7 +208,11 @@ def plan_rates(args, tokens_per_step):
         return sp.SlicingRates(0.2, 0.3, 0.5), budget, "fixed 0.2/0.3/0.5 (BASELINE configs[0])", profile
     wl = sp.Workload(tokens=t_expert, phase=sp.Phase.GENERATION)
     mem = sp.greedy_assign(profile, [layer], wl, budget, n_steps=16)
-    return sp.solve_rcg(profile, layer, wl, mem.per_layer_rgg[0]).rates, budget, source, profile
+    rates = sp.solve_rcg(profile, layer, wl, mem.per_layer_rgg[0]).rates
+    if getattr(args, "force_cc", -1.0) >= 0.0:
+        rates = sp.SlicingRates(args.force_cc, 1.0 - rates.gg - args.force_cc, rates.gg)
+        source += f" (r_CC forced to {args.force_cc}: probe, not the planner's split)"
+    return rates, budget, source, profile
 
 
 # ---------------------------------------------------------------------------
