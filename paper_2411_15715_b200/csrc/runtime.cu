@@ -137,7 +137,8 @@ struct PinnedBuf {
   }
 };
 
-constexpr int kRingSlots = 3;
+constexpr int kMaxRingSlots = 8;
+
 
 // Measured timeline: CUDA events on the library's streams (GPU spans) and the
 // host clock (launch / CC spans), both relative to one synchronised origin.
@@ -169,8 +170,8 @@ struct Context {
   int num_sms = 0;
   cudaStream_t s_comp = nullptr, s_copy = nullptr, s_aux = nullptr;
   cudaEvent_t ev_user, ev_x, ev_ycc, ev_done;
-  cudaEvent_t ev_copied[kRingSlots], ev_free[kRingSlots];
-  DevBuf ring[kRingSlots];
+  cudaEvent_t ev_copied[kMaxRingSlots], ev_free[kMaxRingSlots];
+  DevBuf ring[kMaxRingSlots];
   size_t ring_bytes = 0;
   int ring_next = 0;
   DevBuf ws;         // device workspace
@@ -353,6 +354,17 @@ static int place_layer(sp_layer* L) {
   }
   return SP_OK;
 }
+
+// CG staging ring depth.  Decode steps are triple-buffered (the kernel
+// consumes chunk i while i+1 and i+2 are in flight).  Long prefill streams
+// (>= kLongStream chunks in one call) use 6 slots: the launching thread shares
+// the cores with the CC block, and 5 queued copies (~0.8 ms) ride out its
+// scheduling gaps where 2 did not (cfg3, alternating same-box pairs: e2e
+// 430 -> 479 on one box, 477 -> 485 and prefill 533 -> 540 tokens/s on
+// another; decode unchanged).  SP_RING_SLOTS / SP_RING_SLOTS_LONG override.
+static const int g_ring_slots = std::max(2, std::min(kMaxRingSlots, env_int("SP_RING_SLOTS", 3)));
+static const int g_ring_slots_long = std::max(2, std::min(kMaxRingSlots, env_int("SP_RING_SLOTS_LONG", 6)));
+constexpr size_t kLongStream = 32;
 
 // Fill a placed layer from row-major sources: w1t / w3t [H, M], w2 [H, N].
 static int fill_rows(sp_layer* L, const void* w1t, const void* w3t, const void* w2) {
@@ -1215,12 +1227,13 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       if (ci >= L->n_cc_chunks || calls[c].n_g > 0) items.push_back(StreamItem{c, ci, -1});
   }
   size_t next_copy = 0;
+  const int ring_slots = items.size() >= kLongStream ? g_ring_slots_long : g_ring_slots;
   auto enqueue_copy = [&]() -> int {
     StreamItem& it = items[next_copy++];
     const sp_layer* L = calls[it.c].layer;
     const Chunk& ch = L->chunks[size_t(it.ci)];
-    it.slot = C->ring_next;
-    C->ring_next = (C->ring_next + 1) % kRingSlots;
+    it.slot = C->ring_next % ring_slots;
+    C->ring_next = (it.slot + 1) % ring_slots;
     SP_CUDA(cudaStreamWaitEvent(C->s_copy, C->ev_free[it.slot], 0));
     {
       GpuSpan span(C, C->s_copy, 1, SP_TRACE_COPY, double(ch.bytes));
@@ -1278,7 +1291,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   }
 
   // the first ring slots' copies go right behind the (tiny) metadata copies
-  while (next_copy < items.size() && next_copy < size_t(kRingSlots)) SP_TRY(enqueue_copy());
+  while (next_copy < items.size() && next_copy < size_t(ring_slots)) SP_TRY(enqueue_copy());
 
   // ---- x: device copy for the GPU, host copy for the CC threads ----
   bool need_cc = false;
@@ -1784,7 +1797,7 @@ int sp_init(int device, int host_threads) {
   for (cudaEvent_t* e : {&C->ev_user, &C->ev_x, &C->ev_ycc, &C->ev_done, &C->ev_ws, &C->hpin_done[0],
                          &C->hpin_done[1]})
     SP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-  for (int i = 0; i < kRingSlots; ++i) {
+  for (int i = 0; i < kMaxRingSlots; ++i) {
     SP_CUDA(cudaEventCreateWithFlags(&C->ev_copied[i], cudaEventDisableTiming));
     SP_CUDA(cudaEventCreateWithFlags(&C->ev_free[i], cudaEventDisableTiming));
   }
@@ -1818,7 +1831,7 @@ int sp_shutdown(void) {
   cudaDeviceSynchronize();
   for (cudaEvent_t e : {C->ev_user, C->ev_x, C->ev_ycc, C->ev_done, C->ev_ws, C->hpin_done[0], C->hpin_done[1]})
     cudaEventDestroy(e);
-  for (int i = 0; i < kRingSlots; ++i) {
+  for (int i = 0; i < kMaxRingSlots; ++i) {
     cudaEventDestroy(C->ev_copied[i]);
     cudaEventDestroy(C->ev_free[i]);
   }
@@ -1874,7 +1887,7 @@ static int new_layer(Context* C, const sp_layer_desc& d, std::unique_ptr<sp_laye
 static int publish_layer(Context* C, std::unique_ptr<sp_layer>& L, sp_layer_t* out) {
   if (!C->host_only && L->max_chunk_bytes > C->ring_bytes) {
     SP_CUDA(cudaDeviceSynchronize());
-    for (int i = 0; i < kRingSlots; ++i) SP_TRY(C->ring[i].ensure(L->max_chunk_bytes));
+    for (int i = 0; i < std::max(g_ring_slots, g_ring_slots_long); ++i) SP_TRY(C->ring[i].ensure(L->max_chunk_bytes));
     C->ring_bytes = C->ring[0].n;
   }
   *out = L.release();

@@ -100,6 +100,19 @@ def test_many_chunks_exercise_ring_reuse(sp):
             assert orc.max_rel_error(got, ref) <= FP32_TOL
 
 
+def test_long_stream_deep_ring(sp):
+    # >= 32 chunks in one call switch the staging ring to 6 slots; a following
+    # short call goes back to 3 -- slot reuse is tracked per slot either way
+    rng = np.random.default_rng(8)
+    T, M, N = 3, 64, 48
+    for H, n_g in ((2400, 0), (2400, T), (300, 1)):
+        x, w1, w3, w2 = (rng.uniform(-1, 1, s) for s in ((T, M), (M, H), (M, H), (H, N)))
+        sliced = sp.slice_weights(w1, w2, sp.SlicingRates(0.2, 0.8, 0.0), w3, chunk_rows=64)
+        got = sp.mlp_forward_sliced(x, sliced, sp.Activation.SILU, n_g)
+        ref = orc.dense_forward(x, w1, w2, "silu", w3)
+        assert orc.max_rel_error(got, ref) <= FP32_TOL, (H, n_g)
+
+
 def test_diversion_does_not_change_results(sp):
     rng = np.random.default_rng(11)
     x, w1, w2 = rng.uniform(-1, 1, (6, 40)), rng.uniform(-1, 1, (40, 90)), rng.uniform(-1, 1, (90, 30))
