@@ -610,6 +610,8 @@ static bool use_tc(const sp_layer* L, int64_t T) {
   if (L->d.wdtype != SP_BF16) return false;
   return g_tc_min_tokens_env > 0 ? T >= g_tc_min_tokens_env : T > max_token_tile(L->d.model_dim);
 }
+// SP_CC_FIRST=0: submit the CC block after the first chunk copies, as before
+static const bool g_cc_first = env_int("SP_CC_FIRST", 1) != 0;
 // SP_PREREDUCE=0: leave every partial slice to the finalize (no early reduction)
 static const bool g_prereduce = env_int("SP_PREREDUCE", 1) != 0;
 // SP_HOST_MERGE=0: host-output steps finalize on the GPU like device-output ones
@@ -1211,6 +1213,67 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   SP_CUDA(cudaEventRecord(C->ev_user, user));
   SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_user, 0));
 
+  // ---- x (device copy for the GPU, host copy for the CC threads) and the CC
+  // block, submitted to the coordinator: before the first chunk copies when x is
+  // already on the host (the CC block is the decode step's long pole), else after
+  bool need_cc = false;
+  const void* x_dev = x;
+  const void* x_host = nullptr;
+  bool cc_async = false;
+  bool cc_started = false;
+  std::function<int()> cc_work;
+  auto start_cc = [&]() -> int {
+    cc_started = true;
+    // ---- x: device copy for the GPU, host copy for the CC threads ----
+    for (int c = 0; c < n_calls; ++c)
+      need_cc |= calls[c].layer->d.b1 > 0 && calls[c].tokens - calls[c].n_g > 0;
+    if (host_io) {
+      if (stage_bf16)
+        round_bf16_host(static_cast<const float*>(x_src), reinterpret_cast<uint16_t*>(hp + p_x), T * M);
+      else
+        memcpy(hp + p_x, x, size_t(T) * M * xel);
+      SP_CUDA(cudaMemcpyAsync(dws + o_xdev, hp + p_x, size_t(T) * M * xel, cudaMemcpyHostToDevice,
+                              C->s_comp));
+      x_dev = dws + o_xdev;
+      x_host = stage_bf16 ? static_cast<const void*>(hp + p_x) : x;
+    } else if (need_cc && x_host_ready) {
+      x_host = x_host_ready;  // already read back by the caller (sp_moe_forward): no GPU wait
+    } else if (need_cc) {
+      SP_CUDA(cudaMemcpyAsync(hp + p_x, x, size_t(T) * M * xel, cudaMemcpyDeviceToHost, C->s_comp));
+      SP_CUDA(cudaEventRecord(C->ev_x, C->s_comp));
+      x_host = hp + p_x;
+    }
+
+    // ---- CC block: submitted to the coordinator now, runs while we enqueue ----
+    cc_async = need_cc && !(flags & SP_NO_CC_THREADS);
+    const bool x_on_host_now = host_io || x_host_ready;
+    cc_work = [=]() -> int {
+      if (!x_on_host_now) {
+        const cudaError_t e = cudaEventSynchronize(C->ev_x);
+        if (e != cudaSuccess) return fail(SP_ERR_CUDA, "x copy for the CC block: %s", cudaGetErrorString(e));
+      }
+      for (int c = 0; c < n_calls; ++c) {
+        const double t_cc0 = now_s();
+        const sp_layer* L = calls[c].layer;
+        const int64_t Tcc = calls[c].tokens - calls[c].n_g;
+        if (L->d.b1 <= 0 || Tcc <= 0) continue;
+        const int64_t ldx = round_up(M, kPadElems);
+        C->hscratch.assign(size_t(Tcc * ldx), 0.f);
+        gather_host_x(C->hscratch.data(), ldx, x_host, xdtype, M, calls[c].token_ids, Tcc);
+        std::vector<HostChunk> hc = host_cc_chunks(L);
+        CCProblem pr{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, L->ldn, hc.data(), L->n_cc_chunks,
+                     L->d.b1, C->hscratch.data(), ldx, Tcc, reinterpret_cast<float*>(hp + p_ycc[c])};
+        cc_forward(pr, *C->pool, (flags & SP_NO_CC_THREADS) ? 1 : C->host_threads);
+        host_span(C, 3, SP_TRACE_CC, t_cc0, now_s(), double(L->cc_bytes));
+      }
+      return SP_OK;
+    };
+    if (cc_async) cc_submit(C, cc_work);
+    return SP_OK;
+  };
+  const bool cc_early = g_cc_first && (host_io || x_host_ready);
+  if (cc_early) SP_TRY(start_cc());
+
   // ---- CG chunks (and CC chunks for the n_g diverted rows): the copy stream
   // is the step's bottleneck, so the first ring slots' copies are enqueued
   // before anything else; each later copy right after the kernel that frees its slot.
@@ -1293,54 +1356,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   // the first ring slots' copies go right behind the (tiny) metadata copies
   while (next_copy < items.size() && next_copy < size_t(ring_slots)) SP_TRY(enqueue_copy());
 
-  // ---- x: device copy for the GPU, host copy for the CC threads ----
-  bool need_cc = false;
-  for (int c = 0; c < n_calls; ++c)
-    need_cc |= calls[c].layer->d.b1 > 0 && calls[c].tokens - calls[c].n_g > 0;
-  const void* x_dev = x;
-  const void* x_host = nullptr;
-  if (host_io) {
-    if (stage_bf16)
-      round_bf16_host(static_cast<const float*>(x_src), reinterpret_cast<uint16_t*>(hp + p_x), T * M);
-    else
-      memcpy(hp + p_x, x, size_t(T) * M * xel);
-    SP_CUDA(cudaMemcpyAsync(dws + o_xdev, hp + p_x, size_t(T) * M * xel, cudaMemcpyHostToDevice,
-                            C->s_comp));
-    x_dev = dws + o_xdev;
-    x_host = stage_bf16 ? static_cast<const void*>(hp + p_x) : x;
-  } else if (need_cc && x_host_ready) {
-    x_host = x_host_ready;  // already read back by the caller (sp_moe_forward): no GPU wait
-  } else if (need_cc) {
-    SP_CUDA(cudaMemcpyAsync(hp + p_x, x, size_t(T) * M * xel, cudaMemcpyDeviceToHost, C->s_comp));
-    SP_CUDA(cudaEventRecord(C->ev_x, C->s_comp));
-    x_host = hp + p_x;
-  }
-
-  // ---- CC block: submitted to the coordinator now, runs while we enqueue ----
-  const bool cc_async = need_cc && !(flags & SP_NO_CC_THREADS);
-  const bool x_on_host_now = host_io || x_host_ready;
-  auto cc_work = [=]() -> int {
-    if (!x_on_host_now) {
-      const cudaError_t e = cudaEventSynchronize(C->ev_x);
-      if (e != cudaSuccess) return fail(SP_ERR_CUDA, "x copy for the CC block: %s", cudaGetErrorString(e));
-    }
-    for (int c = 0; c < n_calls; ++c) {
-      const double t_cc0 = now_s();
-      const sp_layer* L = calls[c].layer;
-      const int64_t Tcc = calls[c].tokens - calls[c].n_g;
-      if (L->d.b1 <= 0 || Tcc <= 0) continue;
-      const int64_t ldx = round_up(M, kPadElems);
-      C->hscratch.assign(size_t(Tcc * ldx), 0.f);
-      gather_host_x(C->hscratch.data(), ldx, x_host, xdtype, M, calls[c].token_ids, Tcc);
-      std::vector<HostChunk> hc = host_cc_chunks(L);
-      CCProblem pr{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, L->ldn, hc.data(), L->n_cc_chunks,
-                   L->d.b1, C->hscratch.data(), ldx, Tcc, reinterpret_cast<float*>(hp + p_ycc[c])};
-      cc_forward(pr, *C->pool, (flags & SP_NO_CC_THREADS) ? 1 : C->host_threads);
-      host_span(C, 3, SP_TRACE_CC, t_cc0, now_s(), double(L->cc_bytes));
-    }
-    return SP_OK;
-  };
-  if (cc_async) cc_submit(C, cc_work);
+  if (!cc_started) SP_TRY(start_cc());
 
   // ---- GG blocks (HBM resident): the decode-size calls share one grouped launch ----
   // GG work is off the critical path (the copy stream paces the step), but it
