@@ -212,17 +212,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (lane == 0) {
         const unsigned char* st = smem + size_t(s) * STAGE;
+        if (!g.dbg_no_mma) {
 #pragma unroll
-        for (int kk = 0; kk < (g.dbg_no_mma ? 0 : BK / UK); ++kk) {
-          const uint64_t b = umma_desc(st + NA * A_BYTES + kk * 32, 16, 1024);
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            const uint64_t b = umma_desc(st + NA * A_BYTES + kk * 32, 16, 1024);
 #pragma unroll
-          for (int a = 0; a < NA; ++a) {
-            const uint64_t ad = a_mn ? umma_desc(st + a * A_BYTES + kk * UK * 128, BK * 128, 1024)
-                                     : umma_desc(st + a * A_BYTES + kk * 32, 16, 1024);
-            umma_bf16(tmem + uint32_t(a * NT), ad, b, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+            for (int a = 0; a < NA; ++a) {
+              const uint64_t ad = a_mn ? umma_desc(st + a * A_BYTES + kk * UK * 128, BK * 128, 1024)
+                                       : umma_desc(st + a * A_BYTES + kk * 32, 16, 1024);
+              umma_bf16(tmem + uint32_t(a * NT), ad, b, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+            }
           }
         }
-        umma_commit(&empty[s]);
+        umma_commit(&empty[s]);  // the probe still hands every stage back
         if (kb == kb1 - 1) umma_commit(tmem_full);
       }
       __syncwarp();
