@@ -472,7 +472,11 @@ def run_ours(args):
     clk.armed = False
     clk.stop()
     clocks = clk.summary()
-    e2e_ms, _, _, _ = timed(args.steps, host_io=True)
+    # SP_BENCH_TRACE_E2E=path: also trace the e2e region (probe; the e2e number then carries the trace cost)
+    e2e_trace = os.environ.get("SP_BENCH_TRACE_E2E", "")
+    e2e_ms, _, _, e2e_spans = timed(args.steps, host_io=True, trace=bool(e2e_trace))
+    if e2e_trace and rank == 0:
+        Path(e2e_trace).write_text(json.dumps(e2e_spans))
     value = global_batch / (ms_step * 1e-3)
     e2e_value = global_batch / (e2e_ms * 1e-3)
 

@@ -440,6 +440,8 @@ constexpr int kMaxTileFloats = 16384;  // TT * roundup(M, 256) floats of x <= 64
 // Streamed chunks hide under their own PCIe copy (~150 us for 8 MB), so they
 // run on fewer, fatter CTAs: fewer partial slices for finalize_kernel.
 static const int g_chunk_min_rows = std::max(1, env_int("SP_CHUNK_MIN_ROWS", 16));
+// SP_WIDE_LAST_CHUNK=0: a call's last streamed chunk keeps the chunk grid too
+static const bool g_wide_last_chunk = env_int("SP_WIDE_LAST_CHUNK", 1) != 0;
 
 // CTAs a block of `rows` hidden units is split over (also its partial-slice count).
 static int block_grid(const Context* C, int64_t rows, int min_rows = g_min_rows_per_cta) {
@@ -614,9 +616,9 @@ static bool use_tc(const sp_layer* L, int64_t T) {
 static const bool g_cc_first = env_int("SP_CC_FIRST", 1) != 0;
 // SP_PREREDUCE=0: leave every partial slice to the finalize (no early reduction)
 static const bool g_prereduce = env_int("SP_PREREDUCE", 1) != 0;
-// SP_HOST_MERGE=0: host-output steps finalize on the GPU like device-output ones
-static const bool g_host_merge = env_int("SP_HOST_MERGE", 1) != 0;
-constexpr int64_t kHostMergeMaxElems = int64_t(1) << 16;  // output-row entries x N merged on the host
+// SP_Y_ZERO_COPY=0: small host outputs go through a device buffer and a read-back copy
+static const bool g_y_zero_copy = env_int("SP_Y_ZERO_COPY", 1) != 0;
+constexpr size_t kZeroCopyY = size_t(256) << 10;
 constexpr int kTcMaxSplits = 24;
 // finalize: per-token rows kernel up to this many slices per call, slice groups beyond
 constexpr int kFinRowsMaxSlices = 16;  // split-K output slices a resident tc block may use
@@ -1136,6 +1138,13 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       o_atc(n_calls);
   std::vector<int64_t> ws_ld_a(n_calls);
   std::vector<int> ws_split(n_calls, 0);
+  // Streamed chunks run on few, fat CTAs (they hide under their own copy), except
+  // a call's last one: nothing is left to hide it and the step waits for it.
+  std::vector<int> last_ci(n_calls, -1);
+  for (int c = 0; c < n_calls; ++c)
+    for (int ci = 0; ci < int(calls[c].layer->chunks.size()); ++ci)
+      if (ci >= calls[c].layer->n_cc_chunks || calls[c].n_g > 0) last_ci[c] = ci;
+  auto chunk_min_rows = [&](int c, int ci) { return ci == last_ci[c] && g_wide_last_chunk ? g_min_rows_per_cta : g_chunk_min_rows; };
   int64_t total_rows = 0;
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
@@ -1144,7 +1153,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     ws_split[c] = tc_call ? kTcMaxSplits : 0;
     int64_t slices = block_grid(C, L->h_gg) + 1 + ws_split[c];  // + tc accumulation slice + tc splits
     for (int ci = 0; ci < int(L->chunks.size()); ++ci)
-      if (ci >= L->n_cc_chunks || calls[c].n_g > 0) slices += block_grid(C, L->chunks[ci].rc, g_chunk_min_rows);
+      if (ci >= L->n_cc_chunks || calls[c].n_g > 0) slices += block_grid(C, L->chunks[ci].rc, chunk_min_rows(c, ci));
     o_part[c] = dalloc(size_t(slices) * Te * N * 4);
     const bool tc = tc_call;
     int64_t max_rows = L->h_gg;
@@ -1191,18 +1200,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   const size_t p_x = palloc(size_t(T) * M * xel);
   std::vector<size_t> p_ycc(n_calls);
   for (int c = 0; c < n_calls; ++c) p_ycc[c] = palloc(size_t(calls[c].tokens) * N * 4);
-  // Host output of a small step whose finalize would wait for the host CC block:
-  // the device partials (pre-reduced, read back while the CC block runs) and the
-  // CC partial are merged by the thread that finishes the CC block -- no GPU
-  // launch, kernel and read-back after it.
-  bool any_cc = false;
-  for (int c = 0; c < n_calls; ++c) any_cc |= calls[c].layer->d.b1 > 0 && calls[c].tokens - calls[c].n_g > 0;
-  const bool host_merge = host_io && any_cc && !(flags & SP_NO_CC_THREADS) && g_prereduce && g_host_merge &&
-                          N % 4 == 0 && total_rows * N <= kHostMergeMaxElems;
-  std::vector<size_t> p_dev(n_calls, 0);
-  if (host_merge)
-    for (int c = 0; c < n_calls; ++c) p_dev[c] = palloc(size_t(calls[c].tokens) * N * 4);
-  const size_t p_y = palloc(host_io && !host_merge ? size_t(T) * N * yel : 0);
+  const size_t p_y = palloc(host_io ? size_t(T) * N * yel : 0);
+  // Small host outputs are written by the finalize kernel straight into pinned
+  // host memory (mapped, unified addressing): no read-back copy after it.
+  const bool y_zero_copy = host_io && g_y_zero_copy && size_t(T) * N * yel <= kZeroCopyY;
   const int hb = C->hpin_turn;
   C->hpin_turn ^= 1;
   if (C->hpin_used[hb]) SP_CUDA(cudaEventSynchronize(C->hpin_done[hb]));
@@ -1463,12 +1464,12 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       // a cg_prime block writes only rows [t0, Te) of its slices; the reducer sums every row
       const size_t slice = size_t(Te) * N * 4;
       SP_CUDA(cudaMemsetAsync(ws[c].part + size_t(ws[c].S) * Te * N, 0,
-                              slice * block_grid(C, ch.rc, g_chunk_min_rows), C->s_comp));
+                              slice * block_grid(C, ch.rc, chunk_min_rows(c, it.ci)), C->s_comp));
     }
     {
       GpuSpan span(C, C->s_comp, 2, is_cc ? SP_TRACE_CG_PRIME : SP_TRACE_CG, double(ch.bytes));
       SP_TRY(run_block(C, L, b, x_dev, xdtype, M, ws[c], calls[c].token_ids, Te, t0, Te - t0, C->s_comp,
-                       g_chunk_min_rows));
+                       chunk_min_rows(c, it.ci)));
       span.end();
     }
     SP_CUDA(cudaEventRecord(C->ev_free[it.slot], C->s_comp));
@@ -1488,7 +1489,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   FinalArgs fa{};
   fa.T = int(T);
   fa.N = int(N);
-  fa.out = host_io ? static_cast<void*>(dws + o_ydev) : y;
+  fa.out = y_zero_copy ? static_cast<void*>(hp + p_y) : host_io ? static_cast<void*>(dws + o_ydev) : y;
   fa.odtype = ydtype;
   {
     const int32_t* cs = reinterpret_cast<const int32_t*>(dws + o_csr);
@@ -1523,43 +1524,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   }
   int max_slices = 0;
   for (int c = 0; c < n_calls; ++c) max_slices = std::max(max_slices, fa.c[c].S);
-  if (host_merge) {
-    for (int c = 0; c < n_calls; ++c)
-      if (calls[c].tokens > 0 && fa.c[c].S > 0)
-        SP_CUDA(cudaMemcpyAsync(hp + p_dev[c], ws[c].part, size_t(calls[c].tokens) * N * 4, cudaMemcpyDeviceToHost,
-                                C->s_comp));
-    SP_CUDA(cudaEventRecord(C->hpin_done[hb], C->s_comp));
-  }
   // The tail runs on whichever thread finishes last: this one (GPU work all
   // enqueued) or the CC coordinator (CC block done) -- so finalize is enqueued
   // the moment both are ready, without a thread wake-up in between.
-  auto host_tail = [=]() -> int {
-    const cudaError_t e = cudaEventSynchronize(C->hpin_done[hb]);
-    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "device partial read-back: %s", cudaGetErrorString(e));
-    const double t0 = now_s();
-    const int32_t* cs = reinterpret_cast<const int32_t*>(hp + p_csr);
-    const int32_t* ccall = cs + (T + 1);
-    const int32_t* crow = ccall + total_rows;
-    const float* cgate = reinterpret_cast<const float*>(crow + total_rows);
-    std::vector<float> rowbuf(ydtype == SP_F32 ? 0 : size_t(N));
-    for (int64_t t = 0; t < T; ++t) {
-      float* acc = ydtype == SP_F32 ? static_cast<float*>(y) + t * N : rowbuf.data();
-      std::fill(acc, acc + N, 0.f);
-      for (int e = cs[t]; e < cs[t + 1]; ++e) {
-        const int c = ccall[e], i = crow[e];
-        const float g = cgate[e];
-        const float* dev = fa.c[c].S > 0 ? reinterpret_cast<const float*>(hp + p_dev[c]) + int64_t(i) * N : nullptr;
-        const float* cc = fa.c[c].y_cc && i < fa.c[c].n_cc ? reinterpret_cast<const float*>(hp + p_ycc[c]) + int64_t(i) * N
-                                                           : nullptr;
-        for (int64_t n = 0; n < N; ++n) acc[n] += g * ((dev ? dev[n] : 0.f) + (cc ? cc[n] : 0.f));
-      }
-      if (ydtype != SP_F32) round_bf16_host(acc, static_cast<uint16_t*>(y) + t * N, N);
-    }
-    host_span(C, 3, SP_TRACE_MERGE, t0, now_s(), 0.0);
-    return SP_OK;
-  };
   auto tail = [=]() -> int {
-    if (host_merge) return host_tail();
     if (ycc_copy) {
       // after ws's allocation and the previous forward's finalize (reads these buffers)
       SP_CUDA(cudaStreamWaitEvent(C->s_aux, C->ev_ws, 0));
@@ -1592,7 +1560,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     SP_CUDA(cudaGetLastError());
     span.end();
     ++C->launches;
-    if (host_io)
+    if (host_io && !y_zero_copy)
       SP_CUDA(cudaMemcpyAsync(hp + p_y, dws + o_ydev, size_t(T) * N * yel, cudaMemcpyDeviceToHost, C->s_comp));
     else
       SP_CUDA(cudaEventRecord(C->ev_done, C->s_comp));
@@ -1606,9 +1574,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     if (need_cc) SP_TRY(cc_work());
     SP_TRY(tail());
   }
-  if (host_merge) {
-    // y written by the tail
-  } else if (host_io) {
+  if (host_io) {
     SP_CUDA(cudaStreamSynchronize(C->s_comp));
     memcpy(y, hp + p_y, size_t(T) * N * yel);
   } else {
