@@ -1357,6 +1357,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   // the first ring slots' copies go right behind the (tiny) metadata copies
   while (next_copy < items.size() && next_copy < size_t(ring_slots)) SP_TRY(enqueue_copy());
 
+  // x only on the device: its read-back for the CC block queues behind the first copies
   if (!cc_started) SP_TRY(start_cc());
 
   // ---- GG blocks (HBM resident): the decode-size calls share one grouped launch ----
