@@ -255,88 +255,136 @@ static void axpy_rows(const void* const* rows, int nr, const float* a, int64_t T
 
 // ---------------------------------------------------------------------------
 
-void cc_forward(const CCProblem& p, ThreadPool& pool, int threads) {
-  const int64_t T = p.T;
-  if (p.b1 <= 0 || T <= 0) {
-    for (int64_t i = 0; i < T * p.N; ++i) p.y[i] = 0.f;
-    return;
-  }
-  const int wd = p.wdtype;
-  if (wd == 1 && g_amx && T >= g_amx_min_t && host_has_amx()) return cc_forward_amx(p, pool, threads);
-  const size_t esz = wd == 1 ? 2 : 4;
-  const int64_t k_up = round16(p.M);
-  const int64_t n16 = round16(p.N);  // W2 rows are zero padded to ldn >= roundup(N, 64)
-  const int n_thr = int(std::max<int64_t>(1, std::min<int64_t>(std::min(threads, pool.size()), p.b1)));
+namespace {
 
-  // hidden row -> chunk
-  std::vector<int> chunk_of(size_t(p.b1));
-  for (int c = 0; c < p.n_chunks; ++c)
-    for (int64_t r = 0; r < p.chunks[c].rc; ++r) chunk_of[size_t(p.chunks[c].r0 + r)] = c;
+// One problem's share of a (batched) CC pass: its row blocks and partial slices.
+struct CCPlan {
+  const CCProblem* p;
+  int64_t k_up, n16, slice, nb;
+  int64_t blk0;   // first global block index
+  size_t ybuf0;   // offset of its slices in the shared partial buffer
+  std::vector<int> chunk_of;
+};
 
+CCPlan plan_cc(const CCProblem& p, int n_thr) {
+  CCPlan c{&p, round16(p.M), round16(p.N), 0, 0, 0, 0, {}};
+  c.slice = p.T * c.n16;
   // Hidden rows are processed in blocks claimed dynamically (an atomic
   // cursor), so a preempted or slow thread does not hold up the block: with
   // 16 threads on a shared 16-vCPU host the static split's tail was the CC
   // block's largest jitter.  Each row block accumulates into its own partial
   // slice and the slices are summed in block order -- the result does not
   // depend on which thread ran which block (deterministic).
-  const int64_t slice = T * n16;
-  const int64_t budget = (int64_t(8) << 20) / (slice * 4);  // partial slices within 8 MB
-  int64_t nb = std::min<int64_t>(p.b1, std::max<int64_t>(n_thr, std::min<int64_t>(budget, 8 * n_thr)));
-  nb = std::max<int64_t>(1, nb);
+  const int64_t budget = (int64_t(8) << 20) / (c.slice * 4);  // partial slices within 8 MB
+  c.nb = std::max<int64_t>(1, std::min<int64_t>(p.b1, std::max<int64_t>(n_thr, std::min<int64_t>(budget, 8 * n_thr))));
+  c.chunk_of.resize(size_t(p.b1));
+  for (int k = 0; k < p.n_chunks; ++k)
+    for (int64_t r = 0; r < p.chunks[k].rc; ++r) c.chunk_of[size_t(p.chunks[k].r0 + r)] = k;
+  return c;
+}
+
+// rows [h0, h1) of one problem into its partial slice ybuf
+void cc_rows(const CCPlan& c, int64_t h0, int64_t h1, float* ybuf, float* s, float* a) {
+  const CCProblem& p = *c.p;
+  const int64_t T = p.T;
+  const int wd = p.wdtype;
+  const size_t esz = wd == 1 ? 2 : 4;
+  const void* w2rows[4];
+  std::fill(ybuf, ybuf + c.slice, 0.f);
+  int pend = 0;
+  for (int64_t h = h0; h < h1; ++h) {
+    const HostChunk& ch = p.chunks[c.chunk_of[size_t(h)]];
+    const int64_t off1 = (h - ch.r0) * p.ldm * int64_t(esz);
+    const void* rows[2] = {static_cast<const char*>(ch.w1t) + off1,
+                           p.gated ? static_cast<const char*>(ch.w3t) + off1 : nullptr};
+    if (p.gated) {
+      dot_rows<2>(rows, c.k_up, p.x, p.ldx, T, wd, s);
+      for (int64_t t = 0; t < T; ++t) a[pend * T + t] = act_host(p.act, s[t]) * s[T + t];
+    } else {
+      dot_rows<1>(rows, c.k_up, p.x, p.ldx, T, wd, s);
+      for (int64_t t = 0; t < T; ++t) a[pend * T + t] = act_host(p.act, s[t]);
+    }
+    w2rows[pend++] = static_cast<const char*>(ch.w2) + (h - ch.r0) * p.ldn * int64_t(esz);
+    if (pend == 4 || h + 1 == h1) {
+      axpy_rows(w2rows, pend, a, T, ybuf, c.n16, c.n16, wd);
+      pend = 0;
+    }
+  }
+}
+
+}  // namespace
+
+void cc_forward_batch(const CCProblem* ps, int n, ThreadPool& pool, int threads) {
+  std::vector<CCPlan> plans;
+  int64_t t_max = 1;
+  for (int i = 0; i < n; ++i) {
+    const CCProblem& p = ps[i];
+    if (p.b1 <= 0 || p.T <= 0) {
+      for (int64_t k = 0; k < p.T * p.N; ++k) p.y[k] = 0.f;
+      continue;
+    }
+    if (p.wdtype == 1 && g_amx && p.T >= g_amx_min_t && host_has_amx()) {
+      cc_forward_amx(p, pool, threads);
+      continue;
+    }
+    plans.reserve(size_t(n));
+    const int n_thr = int(std::max<int64_t>(1, std::min<int64_t>(std::min(threads, pool.size()), p.b1)));
+    plans.push_back(plan_cc(p, n_thr));
+    t_max = std::max(t_max, p.T);
+  }
+  if (plans.empty()) return;
+  int64_t blocks = 0, most_rows = 1;
+  size_t floats = 0;
+  for (CCPlan& c : plans) {
+    c.blk0 = blocks;
+    c.ybuf0 = floats;
+    blocks += c.nb;
+    floats += size_t(c.nb * c.slice);
+    most_rows = std::max(most_rows, c.p->b1);
+  }
+  const int n_thr = int(std::max<int64_t>(1, std::min<int64_t>(std::min(threads, pool.size()), most_rows)));
   // persistent across calls (no page faults on fresh mmap'd memory every call)
   // (a thread_local is per thread: the workers below must use this pointer)
   static thread_local std::vector<float> tl_ybufs;
-  tl_ybufs.resize(std::max(tl_ybufs.size(), size_t(nb) * slice));
+  tl_ybufs.resize(std::max(tl_ybufs.size(), floats));
   float* const ybufs = tl_ybufs.data();
   std::atomic<int64_t> cursor{0};
 
   auto rows_pass = [&](int, int) {
-    std::vector<float> s(size_t(2 * T)), a(size_t(4 * T));
-    const void* w2rows[4];
+    std::vector<float> s(size_t(2 * t_max)), a(size_t(4 * t_max));
+    size_t pi = 0;
     for (;;) {
-      const int64_t blk = cursor.fetch_add(1, std::memory_order_relaxed);
-      if (blk >= nb) break;
-      const int64_t h0 = p.b1 * blk / nb, h1 = p.b1 * (blk + 1) / nb;
-      float* ybuf = ybufs + size_t(blk) * slice;
-      std::fill(ybuf, ybuf + slice, 0.f);
-      int pend = 0;
-      for (int64_t h = h0; h < h1; ++h) {
-        const HostChunk& c = p.chunks[chunk_of[size_t(h)]];
-        const int64_t off1 = (h - c.r0) * p.ldm * int64_t(esz);
-        const void* rows[2] = {static_cast<const char*>(c.w1t) + off1,
-                               p.gated ? static_cast<const char*>(c.w3t) + off1 : nullptr};
-        if (p.gated) {
-          dot_rows<2>(rows, k_up, p.x, p.ldx, T, wd, s.data());
-          for (int64_t t = 0; t < T; ++t) a[pend * T + t] = act_host(p.act, s[t]) * s[T + t];
-        } else {
-          dot_rows<1>(rows, k_up, p.x, p.ldx, T, wd, s.data());
-          for (int64_t t = 0; t < T; ++t) a[pend * T + t] = act_host(p.act, s[t]);
-        }
-        w2rows[pend++] = static_cast<const char*>(c.w2) + (h - c.r0) * p.ldn * int64_t(esz);
-        if (pend == 4 || h + 1 == h1) {
-          axpy_rows(w2rows, pend, a.data(), T, ybuf, n16, n16, wd);
-          pend = 0;
-        }
-      }
+      const int64_t g = cursor.fetch_add(1, std::memory_order_relaxed);
+      if (g >= blocks) break;
+      while (g >= plans[pi].blk0 + plans[pi].nb) ++pi;  // blocks are claimed in increasing order
+      const CCPlan& c = plans[pi];
+      const int64_t blk = g - c.blk0, b1 = c.p->b1;
+      cc_rows(c, b1 * blk / c.nb, b1 * (blk + 1) / c.nb, ybufs + c.ybuf0 + size_t(blk) * c.slice, s.data(), a.data());
     }
   };
   pool.run(n_thr, rows_pass);
 
-  auto reduce = [&](int tid, int n) {
-    const int64_t c0 = (n16 / 16) * tid / n * 16;
-    const int64_t c1 = std::min<int64_t>((n16 / 16) * (tid + 1) / n * 16, p.N);
-    if (c1 <= c0) return;
-    std::vector<float> acc(size_t(c1 - c0));
-    for (int64_t t = 0; t < T; ++t) {
-      std::fill(acc.begin(), acc.end(), 0.f);
-      for (int64_t i = 0; i < nb; ++i) {  // block order: deterministic
-        const float* src = ybufs + size_t(i) * slice + t * n16;
-        for (int64_t col = c0; col < c1; ++col) acc[size_t(col - c0)] += src[col];
+  auto reduce = [&](int tid, int nt) {
+    std::vector<float> acc;
+    for (const CCPlan& c : plans) {
+      const CCProblem& p = *c.p;
+      const int64_t c0 = (c.n16 / 16) * tid / nt * 16;
+      const int64_t c1 = std::min<int64_t>((c.n16 / 16) * (tid + 1) / nt * 16, p.N);
+      if (c1 <= c0) continue;
+      acc.resize(size_t(c1 - c0));
+      for (int64_t t = 0; t < p.T; ++t) {
+        std::fill(acc.begin(), acc.end(), 0.f);
+        for (int64_t i = 0; i < c.nb; ++i) {  // block order: deterministic
+          const float* src = ybufs + c.ybuf0 + size_t(i) * c.slice + t * c.n16;
+          for (int64_t col = c0; col < c1; ++col) acc[size_t(col - c0)] += src[col];
+        }
+        std::copy(acc.begin(), acc.end(), p.y + t * p.N + c0);
       }
-      std::copy(acc.begin(), acc.end(), p.y + t * p.N + c0);
     }
   };
   pool.run(threads, reduce);
 }
+
+void cc_forward(const CCProblem& p, ThreadPool& pool, int threads) { cc_forward_batch(&p, 1, pool, threads); }
 
 }  // namespace sp

@@ -63,6 +63,12 @@ struct CCProblem {
 };
 
 void cc_forward(const CCProblem& p, ThreadPool& pool, int threads);
+// Several problems (the active experts of a decode step) in ONE pass: their row
+// blocks share one dynamic queue and one reduce, so the pool joins once per
+// step instead of twice per expert.  Each problem's result is bit-identical to
+// cc_forward's (same blocks, same block-order sums).  AMX-eligible problems run
+// through cc_forward one after another.
+void cc_forward_batch(const CCProblem* ps, int n, ThreadPool& pool, int threads);
 bool host_has_avx512();
 // AMX tile path for bf16 weights and prompt-size token counts (host_cc_amx.cpp);
 // cc_forward dispatches to it when T >= SP_AMX_MIN_T (default 4) and the host

@@ -612,6 +612,8 @@ static bool use_tc(const sp_layer* L, int64_t T) {
   if (L->d.wdtype != SP_BF16) return false;
   return g_tc_min_tokens_env > 0 ? T >= g_tc_min_tokens_env : T > max_token_tile(L->d.model_dim);
 }
+// SP_CC_BATCH=0: one pool pass per call's CC block instead of one per step
+static const bool g_cc_batch = env_int("SP_CC_BATCH", 1) != 0;
 // SP_CC_FIRST=0: submit the CC block after the first chunk copies, as before
 static const bool g_cc_first = env_int("SP_CC_FIRST", 1) != 0;
 // SP_PREREDUCE=0: leave every partial slice to the finalize (no early reduction)
@@ -1253,20 +1255,36 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         const cudaError_t e = cudaEventSynchronize(C->ev_x);
         if (e != cudaSuccess) return fail(SP_ERR_CUDA, "x copy for the CC block: %s", cudaGetErrorString(e));
       }
+      // every call's CC block in one pass of the pool (one join per step, not two per expert)
+      const double t_cc0 = now_s();
+      const int64_t ldx = round_up(M, kPadElems);
+      int64_t rows = 0;
+      double bytes = 0.0;
+      for (int c = 0; c < n_calls; ++c)
+        if (calls[c].layer->d.b1 > 0) rows += std::max<int64_t>(0, calls[c].tokens - calls[c].n_g);
+      C->hscratch.assign(size_t(rows * ldx), 0.f);
+      std::vector<std::vector<HostChunk>> hcs;
+      std::vector<CCProblem> probs;
+      hcs.reserve(size_t(n_calls));
+      int64_t r0 = 0;
       for (int c = 0; c < n_calls; ++c) {
-        const double t_cc0 = now_s();
         const sp_layer* L = calls[c].layer;
         const int64_t Tcc = calls[c].tokens - calls[c].n_g;
         if (L->d.b1 <= 0 || Tcc <= 0) continue;
-        const int64_t ldx = round_up(M, kPadElems);
-        C->hscratch.assign(size_t(Tcc * ldx), 0.f);
-        gather_host_x(C->hscratch.data(), ldx, x_host, xdtype, M, calls[c].token_ids, Tcc);
-        std::vector<HostChunk> hc = host_cc_chunks(L);
-        CCProblem pr{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, L->ldn, hc.data(), L->n_cc_chunks,
-                     L->d.b1, C->hscratch.data(), ldx, Tcc, reinterpret_cast<float*>(hp + p_ycc[c])};
-        cc_forward(pr, *C->pool, (flags & SP_NO_CC_THREADS) ? 1 : C->host_threads);
-        host_span(C, 3, SP_TRACE_CC, t_cc0, now_s(), double(L->cc_bytes));
+        float* xs = C->hscratch.data() + size_t(r0 * ldx);
+        r0 += Tcc;
+        gather_host_x(xs, ldx, x_host, xdtype, M, calls[c].token_ids, Tcc);
+        hcs.push_back(host_cc_chunks(L));
+        probs.push_back(CCProblem{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, L->ldn, hcs.back().data(),
+                                  L->n_cc_chunks, L->d.b1, xs, ldx, Tcc, reinterpret_cast<float*>(hp + p_ycc[c])});
+        bytes += double(L->cc_bytes);
       }
+      const int cc_threads = (flags & SP_NO_CC_THREADS) ? 1 : C->host_threads;
+      if (g_cc_batch)
+        cc_forward_batch(probs.data(), int(probs.size()), *C->pool, cc_threads);
+      else
+        for (const CCProblem& pr : probs) cc_forward(pr, *C->pool, cc_threads);
+      host_span(C, 3, SP_TRACE_CC, t_cc0, now_s(), bytes);
       return SP_OK;
     };
     if (cc_async) cc_submit(C, cc_work);
