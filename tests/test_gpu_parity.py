@@ -302,3 +302,40 @@ def test_grouped_gg_launch_with_many_experts(sp, torch):
     assert err <= BF16_TOL, err
     for e in experts:
         e.layer.release()
+
+
+_CC_BATCH_PROBE = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2411_15715_b200 import _native
+_native.init(0)
+import paper_2411_15715_b200 as sp
+from paper_2411_15715_b200.sliced import SlicedFFN, SlicedMoE
+rng = np.random.default_rng(5)
+E, M, H = 4, 256, 1000
+ws = [tuple(rng.standard_normal(s).astype(np.float32) / 8 for s in ((H, M), (H, M), (M, H))) for _ in range(E)]
+experts = [SlicedFFN(a, c, sp.SlicingRates(0.4, 0.3, 0.3), w3t=b, dtype="bf16", chunk_rows=128) for a, b, c in ws]
+moe = SlicedMoE(experts, rng.standard_normal((M, E)), 2)
+ys = [moe(rng.standard_normal((T, M))) for T in (1, 2, 3)]
+sys.stdout.buffer.write(b"".join(np.ascontiguousarray(y, dtype=np.float32).tobytes() for y in ys))
+"""
+
+
+def test_cc_batch_pass_is_bit_identical_to_per_expert_passes(tmp_path):
+    """cc_forward_batch (one pool pass for every active expert's CC block) must
+    give the same bits as one cc_forward per expert (SP_CC_BATCH=0)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    repo = str(Path(__file__).resolve().parents[1])
+    script = tmp_path / "probe.py"
+    script.write_text(_CC_BATCH_PROBE)
+    outs = []
+    for v in ("0", "1"):
+        env = dict(os.environ, SP_CC_BATCH=v)
+        r = subprocess.run([sys.executable, str(script), repo], env=env, capture_output=True, timeout=300)
+        assert r.returncode == 0, r.stderr.decode()[-2000:]
+        outs.append(r.stdout)
+    assert len(outs[0]) > 0 and outs[0] == outs[1]
