@@ -626,15 +626,34 @@ __global__ void __launch_bounds__(kFinRowsThreads) finalize_rows_kernel(FinalArg
   const int n = (blockIdx.x * kFinRowsThreads + threadIdx.x) * 4;
   if (n >= p.N) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int e = p.entry_start[t]; e < p.entry_start[t + 1]; ++e) {
+  const int e0 = p.entry_start[t], e1 = p.entry_start[t + 1];
+  // the CC partials may sit in mapped host memory (a PCIe round trip each):
+  // issue the first few entries' loads together, before any slice is summed
+  constexpr int kPre = 4;
+  float4 cpre[kPre];
+#pragma unroll
+  for (int q = 0; q < kPre; ++q) {
+    cpre[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e0 + q < e1) {
+      const FinalCall& fc = p.c[p.entry_call[e0 + q]];
+      const int i = p.entry_row[e0 + q];
+      if (fc.y_cc && i < fc.n_cc) cpre[q] = *reinterpret_cast<const float4*>(fc.y_cc + int64_t(i) * p.N + n);
+    }
+  }
+  for (int e = e0; e < e1; ++e) {
     const FinalCall& fc = p.c[p.entry_call[e]];
     const int i = p.entry_row[e];
     const int64_t stride = int64_t(fc.T_e) * p.N;
     const float* base = fc.part + int64_t(i) * p.N + n;
-    // the CC partial may sit in mapped host memory: issue its load first
     const bool cc = fc.y_cc && i < fc.n_cc;
-    const float4 c = cc ? *reinterpret_cast<const float4*>(fc.y_cc + int64_t(i) * p.N + n)
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e - e0 < kPre) {
+#pragma unroll
+      for (int q = 0; q < kPre; ++q)
+        if (q == e - e0) c = cpre[q];
+    } else if (cc) {
+      c = *reinterpret_cast<const float4*>(fc.y_cc + int64_t(i) * p.N + n);
+    }
     float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
     // 8 slice loads in flight per thread, summed in slice order
     int s = 0;
