@@ -48,7 +48,7 @@ sys.path.insert(0, str(ROOT))
 UNIT = "tokens/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
@@ -81,7 +81,7 @@ def parse():
     ap.add_argument("--cpu-sample-steps", type=int, default=6)
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     if args.config == "cfg1":
         args.model_dim, args.hidden_dim, args.dtype = 1024, 3584, "f32"
     elif args.config == "cfg4":  # LLaMA-2-70B dense FFN, column-sharded over the ranks

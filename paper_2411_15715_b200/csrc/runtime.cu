@@ -225,6 +225,20 @@ static std::unique_ptr<Context> g_ctx;
 
 static Context* ctx_or_null() { return g_ctx.get(); }
 
+// Bind the calling thread to the context's device.  The ABI may be entered from
+// any host thread (a Python worker, a rank whose current device was never
+// set); every entry point that touches the library's streams or device memory
+// goes through here first.
+static int bind_device(const Context* C) {
+  if (!C || C->device < 0) return SP_OK;
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != C->device) {
+    const cudaError_t e = cudaSetDevice(C->device);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "cudaSetDevice(%d): %s", C->device, cudaGetErrorString(e));
+  }
+  return SP_OK;
+}
+
 // ---------------------------------------------------------------------------
 // layer placement
 //
@@ -989,6 +1003,10 @@ static void gather_host_x(float* xh, int64_t ldx, const void* x, int xdtype, int
 }
 
 static void cc_coordinator(Context* C) {
+  // this thread may run a forward's tail (finalize launch, event records on the
+  // library's streams), so it must be bound to the context's device: a fresh
+  // host thread starts on device 0, and rank r of a multi-GPU job lives on r
+  if (C->device >= 0) cudaSetDevice(C->device);
   std::unique_lock<std::mutex> lk(C->cc_mu);
   for (;;) {
     C->cc_cv.wait(lk, [&] { return C->cc_stop || (C->cc_pending && C->cc_job); });
@@ -1048,6 +1066,29 @@ static int cc_join_with_tail(Context* C, const std::function<int()>& tail) {
 
 // ---------------------------------------------------------------------------
 // forward
+
+// Error-path cleanup of forward_batch.  A forward that fails after submitting
+// its CC block must not return while the coordinator still runs the job: the
+// job reads the caller's calls / token ids / x and writes the pinned staging
+// half, and a later cc_submit would reset the flags under it (a stale
+// completion then satisfies the next forward's join).  So the destructor,
+// while armed, drops any pending tail, waits for the coordinator to go idle
+// and drains the library's streams (the pinned half's in-flight copies).
+struct ErrorDrain {
+  Context* C;
+  bool armed = true;
+  ~ErrorDrain() {
+    if (!armed) return;
+    {
+      std::unique_lock<std::mutex> lk(C->cc_mu);
+      C->cc_tail = nullptr;
+      C->cc_cv.wait(lk, [&] { return !C->cc_pending; });
+    }
+    cudaStreamSynchronize(C->s_copy);
+    cudaStreamSynchronize(C->s_comp);
+    cudaStreamSynchronize(C->s_aux);
+  }
+};
 
 // fp32 -> bf16 bit patterns, round to nearest even: u + 0x7fff + ((u >> 16) & 1),
 // the same integer arithmetic as the Python fallback (NaNs are not special-cased).
@@ -1211,6 +1252,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   if (C->hpin_used[hb]) SP_CUDA(cudaEventSynchronize(C->hpin_done[hb]));
   SP_TRY(C->hpin[hb].ensure(pin_off));
   char* hp = static_cast<char*>(C->hpin[hb].p);
+  // Any error return from here on leaves no work behind: the CC job (which
+  // reads this call's arguments and writes the pinned half) is joined and the
+  // GPU work already enqueued (copies from the pinned half) is drained.
+  ErrorDrain drain{C};
 
   // ---- stream ordering against the caller ----
   SP_CUDA(cudaEventRecord(C->ev_user, user));
@@ -1593,6 +1638,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     if (need_cc) SP_TRY(cc_work());
     SP_TRY(tail());
   }
+  drain.armed = false;
   if (host_io) {
     SP_CUDA(cudaStreamSynchronize(C->s_comp));
     memcpy(y, hp + p_y, size_t(T) * N * yel);
@@ -1901,6 +1947,7 @@ int sp_layer_create(const sp_layer_desc* desc, const void* w1t, const void* w3t,
   if (desc->gated && !w3t) return fail(SP_ERR_VALUE, "gated layer needs w3t");
   Context* C = ctx_or_null();
   if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  SP_TRY(bind_device(C));
   std::lock_guard<std::mutex> g(C->mu);
   std::unique_ptr<sp_layer> L;
   SP_TRY(new_layer(C, *desc, L));
@@ -1922,6 +1969,7 @@ int sp_layer_image_sizes(sp_layer_t L, size_t* gg_bytes, size_t* host_bytes, int
 
 int sp_layer_export(sp_layer_t L, void* gg_dst, void* host_dst) {
   if (!L) return fail(SP_ERR_VALUE, "NULL layer");
+  SP_TRY(bind_device(ctx_or_null()));
   if (gg_dst && L->gg_bytes) SP_CUDA(cudaMemcpy(gg_dst, L->gg, L->gg_bytes, cudaMemcpyDeviceToHost));
   if (host_dst && L->host_bytes) memcpy(host_dst, L->host, L->host_bytes);
   return SP_OK;
@@ -1933,6 +1981,7 @@ int sp_layer_create_from_images(const sp_layer_desc* desc, const void* gg_img, s
   if (desc->chunk_rows <= 0) return fail(SP_ERR_VALUE, "images need the chunk_rows they were packed with");
   Context* C = ctx_or_null();
   if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  SP_TRY(bind_device(C));
   std::lock_guard<std::mutex> g(C->mu);
   std::unique_ptr<sp_layer> L;
   SP_TRY(new_layer(C, *desc, L));
@@ -1968,6 +2017,7 @@ int sp_layer_load_file(const sp_layer_desc* desc, const char* path, uint64_t gg_
   if (desc->chunk_rows <= 0) return fail(SP_ERR_VALUE, "images need the chunk_rows they were packed with");
   Context* C = ctx_or_null();
   if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  SP_TRY(bind_device(C));
   const int fd = open(path, O_RDONLY);
   if (fd < 0) return fail(SP_ERR_VALUE, "cannot open %s", path);
   std::lock_guard<std::mutex> g(C->mu);
@@ -2010,6 +2060,7 @@ int sp_layer_reslice(sp_layer_t src, int64_t b1, int64_t b2, sp_layer_t* out) {
   if (!src || !out) return fail(SP_ERR_VALUE, "NULL argument");
   Context* C = ctx_or_null();
   if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  SP_TRY(bind_device(C));
   std::lock_guard<std::mutex> g(C->mu);
   sp_layer_desc d = src->d;
   d.b1 = b1;
@@ -2032,6 +2083,7 @@ int sp_layer_destroy(sp_layer_t L) {
   Context* C = ctx_or_null();
   if (C && !C->host_only) {
     std::lock_guard<std::mutex> g(C->mu);
+    bind_device(C);
     cudaStreamSynchronize(C->s_comp);
     cudaStreamSynchronize(C->s_copy);
   }
@@ -2063,6 +2115,7 @@ int sp_forward_batch(const sp_call* calls, int n_calls, const void* x, int xdtyp
   if (C->host_only)
     return fail(SP_ERR_STATE, "host-only context: the GG/CG blocks need a CUDA device (no CPU fallback)");
   if (!calls || !x || !y) return fail(SP_ERR_VALUE, "NULL argument");
+  SP_TRY(bind_device(C));
   std::lock_guard<std::mutex> g(C->mu);
   return forward_batch(C, calls, n_calls, x, xdtype, T, y, ydtype, flags,
                        static_cast<cudaStream_t>(stream));
@@ -2081,6 +2134,7 @@ int sp_moe_forward(const sp_layer_t* layers, int n_experts, const float* router,
   if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
   if (C->host_only)
     return fail(SP_ERR_STATE, "host-only context: the GG/CG blocks need a CUDA device (no CPU fallback)");
+  SP_TRY(bind_device(C));
   std::lock_guard<std::mutex> g(C->mu);
   return moe_forward(C, layers, n_experts, router, top_k, x, xdtype, T, y, ydtype, flags,
                      static_cast<cudaStream_t>(stream));
@@ -2100,6 +2154,9 @@ int sp_cc_forward_host(sp_layer_t L, const void* x, int xdtype, int64_t T, float
                L->d.b1, xh.data(), ldx, T, y_cc};
   Context* C = ctx_or_null();
   if (C && threads != 1) {
+    // the pool is shared with forwards' CC blocks and ThreadPool::run is not
+    // re-entrant: hold the context lock (a forward holds it until its CC join)
+    std::lock_guard<std::mutex> g(C->mu);
     cc_forward(pr, *C->pool, threads > 0 ? threads : C->host_threads);
   } else {
     ThreadPool local(std::max(1, threads));
@@ -2117,6 +2174,7 @@ int sp_round_bf16(const float* src, uint16_t* dst, int64_t n) {
 int sp_trace_enable(int on) {
   Context* C = ctx_or_null();
   if (!C || C->host_only) return fail(SP_ERR_STATE, "sp_init(device) has not been called");
+  SP_TRY(bind_device(C));
   std::lock_guard<std::mutex> g(C->mu);
   Trace& tr = C->trace;
   SP_CUDA(cudaDeviceSynchronize());
@@ -2152,6 +2210,7 @@ int sp_trace_fetch(sp_trace_record* out, int* n) {
   Context* C = ctx_or_null();
   if (!C || C->host_only) return fail(SP_ERR_STATE, "sp_init(device) has not been called");
   if (!n) return fail(SP_ERR_VALUE, "n is NULL");
+  SP_TRY(bind_device(C));
   std::lock_guard<std::mutex> g(C->mu);
   Trace& tr = C->trace;
   const int have = int(tr.spans.size());

@@ -21,7 +21,7 @@ from typing import Callable, Mapping, Sequence
 import numpy as np
 
 from .errors import ShapeMismatch
-from .sliced import CallSpec, MoEDispatch, forward_calls, route_topk
+from .sliced import CallSpec, MoEDispatch, forward_calls, moe_route
 
 
 def owner_of(expert: int, world: int) -> int:
@@ -34,9 +34,11 @@ def local_experts(n_experts: int, rank: int, world: int) -> list[int]:
 
 
 def route_local(x_host: np.ndarray, router_w: np.ndarray, top_k: int, owned: Sequence[int]):
-    """Top-k routing of every token (fp64, ties -> lower expert id), restricted
-    to the owned experts: [(expert, token_rows int32, gates float32)]."""
-    ids, gates = route_topk(np.asarray(x_host, dtype=np.float64) @ router_w, top_k)
+    """Top-k routing of every token through the runtime's router (sp_moe_route:
+    fp64 logits over the fp32 router, ties -> lower expert id -- the same
+    routine sp_moe_forward runs), restricted to the owned experts:
+    [(expert, token_rows int32, gates float32)]."""
+    ids, gates = moe_route(np.asarray(x_host, dtype=np.float32), router_w, top_k)
     plan = []
     for e in owned:
         rows, slots = np.nonzero(ids == e)
@@ -63,7 +65,7 @@ class ExpertParallelMoE:
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.router_w = np.asarray(router_w, dtype=np.float64)
+        self.router_w = np.ascontiguousarray(router_w, dtype=np.float32)  # as sp_moe_route holds it
         if self.router_w.shape[1] != n_experts:
             raise ShapeMismatch("router_w must have one column per expert")
         self.top_k = int(top_k)

@@ -396,7 +396,13 @@ class SlicedWeights:
 
     def placed(self, activation, device: int | None = None) -> NativeLayer:
         act = _act_name(activation)
-        layer = self._placed.get(act)
+        # the library binds one device per process: a layer placed on one GPU is
+        # never silently reused for inputs on another
+        bound = nat.current_device()
+        if device is not None and bound is not None and device != bound:
+            raise ValueError(f"input is on cuda:{device} but this process's sliced layers live on cuda:{bound}")
+        key = (act, device if device is not None else bound)
+        layer = self._placed.get(key)
         if layer is None:
             w1 = np.concatenate(self.w1_blocks, axis=1)
             w2 = np.concatenate(self.w2_blocks, axis=0)
@@ -404,7 +410,7 @@ class SlicedWeights:
             b1, b2 = self.boundaries
             layer = NativeLayer(w1.T, w2, b1, b2, act, None if w3 is None else w3.T,
                                 dtype=self.dtype, chunk_rows=self.chunk_rows, device=device)
-            self._placed[act] = layer
+            self._placed[(act, nat.current_device())] = layer
         return layer
 
 
@@ -587,7 +593,8 @@ def _transpose(a):
 
 
 def route_topk(logits: np.ndarray, k: int) -> tuple[np.ndarray, np.ndarray]:
-    """Top-k expert ids (ties -> lower id) and the softmax over the k logits."""
+    """Top-k expert ids (ties -> lower id) and the softmax over the k logits of
+    precomputed logits (planning helpers; MoE layers route with ``moe_route``)."""
     logits = np.asarray(logits, dtype=np.float64)
     ids = np.argsort(-logits, axis=1, kind="stable")[:, :k]
     top = np.take_along_axis(logits, ids, axis=1)
@@ -596,8 +603,11 @@ def route_topk(logits: np.ndarray, k: int) -> tuple[np.ndarray, np.ndarray]:
 
 
 def moe_route(x, router_w, top_k: int) -> tuple[np.ndarray, np.ndarray]:
-    """The runtime's router (libsliced sp_moe_route): fp64 logits x @ router_w,
-    top-k with ties to the lower expert id, softmax over the k logits."""
+    """The runtime's router (libsliced sp_moe_route): fp64 logits x @ router_w
+    with the router held in fp32, top-k with ties to the lower expert id,
+    softmax over the k logits.  Every MoE path (sp_moe_forward, SlicedMoE.plan,
+    expert_parallel.route_local) routes through this one routine, so a token
+    picks the same experts whichever path runs it."""
     if getattr(x, "dtype", None) == np.uint16:  # bf16 bit patterns
         xh, code = np.ascontiguousarray(x), nat.SP_BF16
     else:
@@ -677,13 +687,13 @@ class SlicedMoE:
 
     def __init__(self, experts: Sequence[SlicedFFN], router_w, top_k: int = 2):
         self.experts = list(experts)
-        self.router_w = np.asarray(router_w, dtype=np.float64)  # [M, E]
+        self.router_w = np.ascontiguousarray(router_w, dtype=np.float32)  # [M, E], as sp_moe_route holds it
         if self.router_w.shape[1] != len(self.experts):
             raise ShapeMismatch("router_w must have one column per expert")
         self.top_k = int(top_k)
 
     def plan(self, x_host: np.ndarray, n_g: dict[int, int] | None = None) -> list[CallSpec]:
-        ids, gates = route_topk(np.asarray(x_host, dtype=np.float64) @ self.router_w, self.top_k)
+        ids, gates = moe_route(np.asarray(x_host, dtype=np.float32), self.router_w, self.top_k)
         calls = []
         for e in range(len(self.experts)):
             rows, slots = np.nonzero(ids == e)

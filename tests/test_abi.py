@@ -152,3 +152,32 @@ def test_native_bf16_cast_matches_numpy_rule():
     u = x.view(np.uint32).astype(np.uint64)
     ref = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
     assert np.array_equal(to_bf16_bits(x), ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gated", [True, False])
+def test_amx_cc_kernel_on_the_gpu_box(gated):
+    """The AMX tile kernel (host_cc_amx.cpp) runs every prompt-row CC block on
+    the GPU box; checked directly here (the host-only fixture above skips when a
+    GPU is present).  Rows >= 4 take the AMX path; a bf16 hidden activation as
+    on the tensor cores.  Also through a whole forward (CC block only, host
+    threads) at Mixtral-like widths."""
+    from paper_2411_15715_b200.sliced import CallSpec, NativeLayer, forward_calls
+
+    if not host_has_amx():
+        pytest.skip("this host has no AMX (amx_bf16)")
+    nat.init(0)
+    rng = np.random.default_rng(31 + gated)
+    q = orc.bf16_round
+    for M, H, N, T in ((256, 640, 192, 4), (512, 1000, 256, 16), (1024, 2048, 1024, 33), (4096, 1024, 4096, 64)):
+        w1, w3 = rng.uniform(-1, 1, (M, H)) / 8, rng.uniform(-1, 1, (M, H)) / 8
+        w2, x = rng.uniform(-1, 1, (H, N)) / 8, rng.uniform(-1, 1, (T, M))
+        lay = NativeLayer(w1.T, w2, H, H, "silu", w3.T if gated else None, dtype="bf16", chunk_rows=128)
+        ref_h = orc.dense_forward_bf16_hidden(q(x), q(w1), q(w2), "silu", q(w3) if gated else None)
+        ref = orc.dense_forward(q(x), q(w1), q(w2), "silu", q(w3) if gated else None)
+        got = lay.cc_forward_host(x, threads=0)
+        assert orc.max_rel_error(got, ref_h) <= 5e-4, (M, H, N, T)
+        assert orc.max_rel_error(got, ref) <= 1e-2, (M, H, N, T)
+        y = forward_calls([CallSpec(lay)], x.astype(np.float32))  # CC block on the pool inside a forward
+        assert orc.max_rel_error(np.asarray(y), ref) <= 1e-2, (M, H, N, T)
+        lay.release()

@@ -1,0 +1,113 @@
+"""Runtime robustness on the GPU: a forward that fails after its CC block was
+submitted leaves nothing running (the next forward is exact), the CC
+coordinator thread runs forwards' tails on the context's device, and the
+placed-layer cache of the reference API is keyed by device."""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from oracle import sliced_forward as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    assert torch.cuda.is_available()
+    from paper_2411_15715_b200 import _native
+
+    _native.init(0)
+    return torch
+
+
+def test_error_after_cc_submit_drains_and_next_forward_is_exact(torch):
+    """A bf16 layer with out_dim 9000 > the GEMV's 8192-column limit fails in
+    its GG launch -- after the host-I/O forward submitted its CC block to the
+    coordinator.  The call must raise, and forwards after it (same staging
+    halves, same coordinator) must be exact."""
+    from paper_2411_15715_b200 import errors
+    from paper_2411_15715_b200.sliced import NativeLayer, SlicedFFN
+
+    rng = np.random.default_rng(3)
+    M, H, N = 128, 512, 9000
+    bad = NativeLayer(rng.standard_normal((H, M)) / 8, rng.standard_normal((H, N)) / 8, 128, 256, "silu",
+                      dtype="bf16", chunk_rows=64)
+    M2, H2 = 256, 768
+    w1t, w3t, w2t = (rng.standard_normal(s).astype(np.float32) / 8 for s in ((H2, M2), (H2, M2), (M2, H2)))
+    good = SlicedFFN(w1t, w2t, None, w3t=w3t, dtype="bf16", boundaries=(200, 400), chunk_rows=64)
+    q = orc.bf16_round
+    from paper_2411_15715_b200.sliced import CallSpec, forward_calls
+
+    for i in range(3):
+        with pytest.raises((errors.NativeError, ValueError)):
+            forward_calls([CallSpec(bad)], rng.standard_normal((1, M)).astype(np.float32))
+        x = rng.standard_normal((2, M2)).astype(np.float32)
+        ref = orc.dense_forward(q(x), q(w1t.T), q(w2t.T), "silu", q(w3t.T))
+        assert orc.max_rel_error(np.asarray(good(x)), ref) <= 1e-2, i
+        xd = torch.from_numpy(x).cuda().to(torch.bfloat16)
+        assert orc.max_rel_error(good(xd).float().cpu().numpy(), ref) <= 1e-2, i
+    bad.release()
+    good.layer.release()
+
+
+_DEVICE_PROBE = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+dev = int(sys.argv[2])
+import torch
+torch.cuda.set_device(0)          # the caller's current device is NOT the library's
+from paper_2411_15715_b200 import _native
+_native.init(dev)
+from paper_2411_15715_b200.sliced import SlicedFFN
+from oracle import sliced_forward as orc
+rng = np.random.default_rng(1)
+M, H = 256, 1024
+w1t, w3t, w2t = (rng.standard_normal(s).astype(np.float32) / 8 for s in ((H, M), (H, M), (M, H)))
+f = SlicedFFN(w1t, w2t, None, w3t=w3t, dtype="bf16", boundaries=(300, 600), chunk_rows=64, device=dev)
+q = orc.bf16_round
+for T in (1, 3, 20):
+    x = rng.standard_normal((T, M)).astype(np.float32)
+    ref = orc.dense_forward(q(x), q(w1t.T), q(w2t.T), "silu", q(w3t.T))
+    err = orc.max_rel_error(np.asarray(f(x)), ref)
+    xd = torch.from_numpy(x).to(f"cuda:{dev}").to(torch.bfloat16)
+    with torch.cuda.device(dev):
+        err = max(err, orc.max_rel_error(f(xd).float().cpu().numpy(), ref))
+    assert err <= 1e-2, (T, err)
+print("ok", dev)
+"""
+
+
+def test_last_device_context_runs_tails_on_its_device(torch, tmp_path):
+    """sp_init on the last visible device while the calling thread's current
+    device is 0: the CC coordinator (which enqueues the finalize when the CC
+    block ends last) must be bound to the context's device.  On a one-GPU box
+    this is device 0 and checks the same path; with more GPUs, device N-1."""
+    dev = torch.cuda.device_count() - 1
+    script = tmp_path / "probe.py"
+    script.write_text(_DEVICE_PROBE)
+    r = subprocess.run([sys.executable, str(script), str(ROOT), str(dev)], capture_output=True, text=True,
+                       timeout=300, env=dict(os.environ))
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert f"ok {dev}" in r.stdout
+
+
+def test_reference_api_layer_cache_is_keyed_by_device(torch):
+    import paper_2411_15715_b200 as sp
+
+    rng = np.random.default_rng(9)
+    x, w1, w2 = rng.uniform(-1, 1, (2, 16)), rng.uniform(-1, 1, (16, 40)), rng.uniform(-1, 1, (40, 8))
+    sliced = sp.slice_weights(w1, w2, sp.SlicingRates(0.25, 0.25, 0.5))
+    y = sp.mlp_forward_sliced(x, sliced, sp.Activation.SILU)
+    assert orc.max_rel_error(y, orc.dense_forward(x, w1, w2, "silu")) <= 1e-5
+    assert len(sliced._placed) == 1 and next(iter(sliced._placed))[1] == 0
+    with pytest.raises(ValueError, match="cuda:1"):
+        sliced.placed(sp.Activation.SILU, device=1)
