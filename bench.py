@@ -78,7 +78,10 @@ def parse(argv=None):
     ap.add_argument("--experts", type=int, default=8)
     ap.add_argument("--top-k", type=int, default=2)
     ap.add_argument("--profile", default=str(ROOT / "profiles" / "b200_decode.json"))
-    ap.add_argument("--cpu-sample-steps", type=int, default=6)
+    ap.add_argument("--cpu-sample-steps", type=int, default=20, help="cpu_baseline: at least this many steps")
+    ap.add_argument("--cpu-sample-s", type=float, default=10.0, help="cpu_baseline: and at least this much CPU work")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="spawn / rendezvous / barrier only (CPU test of the multi-rank launch path)")
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
@@ -203,10 +206,11 @@ def plan_rates(args, tokens_per_step):
         n_gemms, t_expert = 3, max(1, tokens_per_step)
     profile, source = load_profile(decode_profile_for(args.profile, t_expert))
     layer = sp.LayerSpec(args.model_dim, hidden, n_gemms=n_gemms, precision=sp.Precision.FP16)
+    wl = sp.Workload(tokens=t_expert, phase=sp.Phase.GENERATION)
+    args.plan_layer, args.plan_workload = layer, wl  # what predict_step() evaluates
     budget = args.budget_frac * layer.layer_bytes
     if args.config == "cfg1":
         return sp.SlicingRates(0.2, 0.3, 0.5), budget, "fixed 0.2/0.3/0.5 (BASELINE configs[0])", profile
-    wl = sp.Workload(tokens=t_expert, phase=sp.Phase.GENERATION)
     mem = sp.greedy_assign(profile, [layer], wl, budget, n_steps=16)
     rates = sp.solve_rcg(profile, layer, wl, mem.per_layer_rgg[0]).rates
     if getattr(args, "force_cc", -1.0) >= 0.0:
@@ -215,29 +219,87 @@ def plan_rates(args, tokens_per_step):
     return rates, budget, source, profile
 
 
+def predict_step(args, rates, profile) -> dict:
+    """The planner's own prediction of one step on the profile it planned with:
+    stage times (pipeline.py:143-167), the Eq. 5 recurrence over the step's
+    n_gemms GEMMs (pipeline.py:237-260) and its Gantt rows (pipeline.py:347-364),
+    per stream busy time next to t_fin."""
+    import paper_2411_15715_b200 as sp
+
+    layer, wl = args.plan_layer, args.plan_workload
+    stage = sp.stage_times_generation(profile, layer, wl, rates)
+    tl = sp.evaluate_recurrence(stage, layer.n_gemms)
+    return {"t_fin_s": tl.t_fin, "case": tl.case_label.value, "n_gemms": layer.n_gemms,
+            "busy_s": {"transfer": stage.transfer_s * layer.n_gemms, "gpu": stage.gpu_s * layer.n_gemms,
+                       "cpu": stage.cpu_s * layer.n_gemms, "launch": stage.launch_s * layer.n_gemms},
+            "gantt": sp.timeline_records(stage, tl)}
+
+
 # ---------------------------------------------------------------------------
 # clocks
 
 
 class ClockSampler:
+    """SM clock and clock-event reasons sampled DURING the timed region: NVML
+    every 5 ms from a thread (a decode region lasts ~0.2-0.4 s, far below the
+    100 ms granularity of ``nvidia-smi -lms``), nvidia-smi as the fallback."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    # nvmlClocksEventReason* bits, in NAMES order
+    BITS = [0x8, 0x40, 0x20, 0x4]
+    PERIOD_S = 0.005
 
     def __init__(self, device=0):
         self.rows, self.proc, self.device, self.armed = [], None, device, False
         self.first = threading.Event()
+        self.nvml, self.handle, self.stop_ev, self.source = None, None, threading.Event(), "unsampled"
 
     def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            from paper_2411_15715_b200.placement import pci_bus_id
+
+            bid = pci_bus_id(self.device)
+            try:
+                self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(bid.encode() if bid else b"")
+            except Exception:
+                self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.nvml = pynvml
+            self.max_sm = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+            self.source = f"nvml every {self.PERIOD_S * 1e3:g} ms"
+            threading.Thread(target=self._poll, daemon=True).start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
             self.first.wait(timeout=10)
+            self.source = "nvidia-smi -lms 100"
         except FileNotFoundError:
             self.proc = None
         return self
+
+    def _poll(self):
+        nv = self.nvml
+        reason_fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop_ev.is_set():
+            if self.armed:
+                try:
+                    sm = float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM))
+                    r = int(reason_fn(self.handle))
+                    self.rows.append([str(sm), str(self.max_sm)] +
+                                     ["Active" if r & b else "Not Active" for b in self.BITS])
+                except Exception:
+                    pass
+            time.sleep(self.PERIOD_S)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -248,42 +310,60 @@ class ClockSampler:
                     self.rows.append(parts)
 
     def stop(self):
+        self.stop_ev.set()
         if self.proc:
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0,
+                    "source": self.source}
         num = lambda v: float(v) if v.replace(".", "").isdigit() else None  # noqa: E731
         sm = [v for v in (num(r[0]) for r in self.rows) if v is not None]
         mx = [v for v in (num(r[1]) for r in self.rows) if v is not None]
         reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:]) if v.lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": self.source}
 
 
 # ---------------------------------------------------------------------------
 # CPU reference (oracle port of slicing_kernel.py) -- baseline only
 
 
-def cpu_reference_sample(args, rates, steps, warmup=1):
-    """fp64 numpy sliced forward (the reference algorithm) of `batch` tokens
-    through top-k SwiGLU experts; two fp64 expert weight sets (> L3) reused
-    across steps.  Returns (tokens/s, s/step, description, threads)."""
+def blas_info() -> tuple[int, list]:
+    """(BLAS threads, threadpoolctl.threadpool_info() BLAS entries)."""
+    try:
+        import threadpoolctl
+
+        info = [{k: i.get(k) for k in ("user_api", "internal_api", "num_threads", "version", "architecture")}
+                for i in threadpoolctl.threadpool_info() if i.get("user_api") == "blas"]
+        return max((i["num_threads"] or 1 for i in info), default=os.cpu_count() or 1), info
+    except Exception:
+        return os.cpu_count() or 1, []
+
+
+def cpu_reference_sample(args, rates, steps, warmup=1, tokens=None, min_s=0.0, max_steps=None):
+    """fp64 numpy sliced forward (the reference algorithm, slicing_kernel.py:97-124)
+    of `tokens` tokens (default: the global batch) through top-k SwiGLU experts;
+    two fp64 expert weight sets (> L3) reused across steps.  Times at least
+    `steps` steps and keeps going until `min_s` seconds of CPU work (bounded by
+    `max_steps`).  Returns a dict: tokens/s over the whole sample, best and
+    median per-step tokens/s, step times, threads and the BLAS pool."""
     import torch
 
     from oracle import sliced_forward as orc
 
     M, H = args.model_dim, args.hidden_dim
+    tokens = tokens or args.batch
     torch.manual_seed(0)
     sets = [tuple((torch.randn(*s) / 64).double().numpy() for s in ((M, H), (M, H), (H, M)))
             for _ in range(min(2, args.top_k))]
-    x = np.random.default_rng(0).standard_normal((args.batch, M))
+    x = np.random.default_rng(0).standard_normal((tokens, M))
     gates = np.full(args.top_k, 1.0 / args.top_k)
 
     def step():
-        y = np.zeros((args.batch, M))
+        y = np.zeros((tokens, M))
         for k in range(args.top_k):
             w1, w3, w2 = sets[k % len(sets)]
             y += gates[k] * orc.sliced_forward(x, w1, w2, "silu", rates.cc, rates.cg, w3)
@@ -291,20 +371,20 @@ def cpu_reference_sample(args, rates, steps, warmup=1):
 
     for _ in range(warmup):
         step()
-    t0 = time.perf_counter()
-    for _ in range(steps):
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < steps or (time.perf_counter() - t_all < min_s and len(times) < (max_steps or 10 ** 9)):
+        t0 = time.perf_counter()
         step()
-    dt = (time.perf_counter() - t0) / steps
-    try:
-        import threadpoolctl
-
-        threads = max(i.get("num_threads", 1) for i in threadpoolctl.threadpool_info() if i.get("user_api") == "blas")
-    except Exception:
-        threads = os.cpu_count()
-    desc = (f"{steps} steps x {args.batch} token(s) x {args.top_k} experts, fp64 numpy/OpenBLAS "
-            f"(slicing_kernel.py:97-124 as written), rates cc={rates.cc:.4f} cg={rates.cg:.4f} gg={rates.gg:.4f}, "
-            f"2 fp64 expert weight sets")
-    return args.batch / dt, dt, desc, threads
+        times.append(time.perf_counter() - t0)
+    total = time.perf_counter() - t_all
+    threads, info = blas_info()
+    desc = (f"{len(times)} steps x {tokens} token(s) x {args.top_k} experts ({total:.1f} s of CPU work), fp64 "
+            f"numpy/OpenBLAS (slicing_kernel.py:97-124 as written), rates cc={rates.cc:.4f} cg={rates.cg:.4f} "
+            f"gg={rates.gg:.4f}, 2 fp64 expert weight sets")
+    return {"value": tokens * len(times) / total, "best": tokens / min(times), "median": tokens / float(np.median(times)),
+            "s_per_step": total / len(times), "steps": len(times), "threads": threads, "threadpool": info,
+            "sample": desc}
 
 
 # ---------------------------------------------------------------------------
@@ -319,42 +399,68 @@ def ncu_traffic(args):
     return json.loads(f.read_text()).get(f"{args.config}_gg_launch_bytes")
 
 
+def rank_device(local_rank: int) -> int:
+    """CUDA device of a local rank: one GPU per rank; every rank on cuda:0
+    under SP_BENCH_ONE_GPU=1 (multi-rank plumbing on a one-GPU box)."""
+    return 0 if os.environ.get("SP_BENCH_ONE_GPU") == "1" else local_rank
+
+
 def dist_env():
     return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
 def base_config(args, rates, global_batch, world):
+    """The config both arms print (identical dicts, so the driver's same-config
+    check compares like with like)."""
+    from paper_2411_15715_b200.sliced import split_boundaries
+
     wl = {"cfg1": "cfg1-1024x3584-moe-ffn-decode", "cfg2": "mixtral-8x7b-moe-ffn-decode",
           "cfg4": "llama2-70b-dense-ffn-decode-colsharded",
           "cfg5": f"{'phimoe' if args.moe == 'phimoe' else 'mixtral-8x22b'}-moe-ffn-decode-ep"}.get(args.config, args.config)
+    hidden = getattr(args, "shard_hidden", args.hidden_dim)
+    b1, b2 = split_boundaries(hidden, rates)
     return {"workload": wl,
             "model_dim": args.model_dim, "hidden_dim": args.hidden_dim, "experts": args.experts,
             "top_k": args.top_k, "batch_per_gpu": args.batch, "global_batch": global_batch,
             "parallelism": (f"col{world}" if args.config == "cfg4" else f"ep{world}") if world > 1 else "single",
-            "rates": {"cc": rates.cc, "cg": rates.cg, "gg": rates.gg}}
+            "rates": {"cc": rates.cc, "cg": rates.cg, "gg": rates.gg},
+            "block_widths": [b1, b2 - b1, hidden - b2], "budget_frac": args.budget_frac,
+            "l2": "inputs larger than L2: the experts' GG blocks (>1 GB) rotate with routing"}
 
 
 def run_reference(args):
-    world, rank, _ = dist_env()
+    """The reference arm: the reference's CPU algorithm (the oracle port of
+    slicing_kernel.py:97-124, fp64 numpy, every host thread) on this arm's
+    config -- the same global batch per step as the GPU arm at N ranks, planned
+    with rank 0's rates.  Under torchrun only rank 0 runs and prints."""
+    world, rank, local = dist_env()
     if rank != 0:
         return
+    from paper_2411_15715_b200.placement import bind_rank
+
+    # plan exactly as rank 0 of the GPU arm does (its host-thread share), run on every core
+    bind_rank(0, world, device_of=rank_device, apply=False)
+    if args.config == "cfg4":
+        from paper_2411_15715_b200.expert_parallel import column_shard
+
+        lo, hi = column_shard(args.hidden_dim, 0, world)
+        args.shard_hidden = hi - lo
     rates, _, _, _ = plan_rates(args, args.batch)
-    # every host thread for the reference's BLAS, also under torchrun (which
-    # exports OMP_NUM_THREADS=1 to each rank)
+    global_batch = args.batch * world
     from threadpoolctl import threadpool_limits
 
     with threadpool_limits(limits=os.cpu_count(), user_api="blas"):
-        for _ in range(args.warmup):
-            cpu_reference_sample(args, rates, 1, warmup=0)
-        tps, dt, desc, threads = cpu_reference_sample(args, rates, args.steps, warmup=0)
+        # the whole layer (every rank's experts / column shards) for the global batch
+        r = cpu_reference_sample(args, rates, args.steps, warmup=args.warmup, tokens=global_batch)
     line = {
-        "impl": "reference", "metric": metric_name(args), "value": tps, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "impl": "reference", "metric": metric_name(args), "value": r["value"], "unit": UNIT, "n_gpus": world,
+        "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["s_per_step"] * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": base_config(args, rates, args.batch, 1),
-        "cpu_baseline": {"value": tps, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
-        "e2e": {"value": tps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": base_config(args, rates, global_batch, world),
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["threads"], "kind": "port",
+                         "sample": r["sample"], "best": r["best"], "median": r["median"], "threadpool": r["threadpool"]},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -384,24 +490,30 @@ def run_ours(args):
     from paper_2411_15715_b200 import _native as nat
     from paper_2411_15715_b200.expert_parallel import ExpertParallelMoE, local_experts
 
+    from paper_2411_15715_b200.placement import bind_rank
+
     world, rank, local = dist_env()
     # SP_BENCH_ONE_GPU=1 (test plumbing): every rank on cuda:0 with gloo, so the
     # multi-rank bench path runs on a one-GPU box; production is one GPU per rank, NCCL
     one_gpu = os.environ.get("SP_BENCH_ONE_GPU") == "1"
-    if one_gpu:
-        local = 0
-    device = torch.device("cuda", local)
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    dev_index = rank_device(local)
+    device = torch.device("cuda", dev_index)
     torch.cuda.set_device(device)
+    # this rank's share of its GPU's NUMA node (CPU mask + preferred memory),
+    # before sp_init creates the CC pool and before any pinned weight is placed
+    placement = bind_rank(local, local_world, device_of=rank_device)
     dist = None
+    backend = None
     if world > 1:
         import torch.distributed as dist
 
-        os.environ.setdefault("SP_HOST_THREADS", str(max(1, (os.cpu_count() or 16) // world)))
+        backend = "gloo" if one_gpu else "nccl"
         if one_gpu:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=device)
-    nat.init(local)
+    nat.init(dev_index)
 
     B = args.batch
     global_batch = B * world
@@ -491,9 +603,9 @@ def run_ours(args):
     gg_dt = float(np.mean([s["end_s"] - s["start_s"] for s in gg])) if gg else 0.0
     gg_gbs = gg_bytes / gg_dt / 1e9 if gg_dt else 0.0
     # the same launches timed on the device itself (first CTA start -> last CTA
-    # end, %globaltimer): the CUDA-event span above also holds the launch's
-    # front-end latency, ~23 us longer while the copy engine saturates the link
-    # (scripts/probes/launch_latency.cu)
+    # end, %globaltimer).  A timing event recorded while copy-engine H2D traffic
+    # saturates the link costs ~23 us of stream time (scripts/probes/event_span.cu),
+    # which is why the grouped GG launch runs behind the last chunk kernel.
     gg_dev = [s["dev_s"] for s in gg if s.get("dev_s", 0) > 0]
     gg_dev_dt = float(np.mean(gg_dev)) if gg_dev else 0.0
     cp_bytes = sum(s["bytes"] for s in cp)
@@ -521,18 +633,20 @@ def run_ours(args):
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        tps, dt, desc, threads = cpu_reference_sample(args, rates, args.cpu_sample_steps)
-        cpu = {"value": tps, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
+        from threadpoolctl import threadpool_limits
+
+        with threadpool_limits(limits=os.cpu_count(), user_api="blas"):
+            r = cpu_reference_sample(args, rates, args.cpu_sample_steps, min_s=args.cpu_sample_s, max_steps=2000)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["threads"], "kind": "port", "sample": r["sample"],
+               "best": r["best"], "median": r["median"], "threadpool": r["threadpool"]}
 
     first = next(iter(experts.values())) if experts else None
     xel = 2 if args.dtype == "bf16" else 4
     config = base_config(args, rates, global_batch, world)
-    config.update({
-        "block_widths": first.block_widths if first else None,
-        "gpu_budget_bytes": budget, "budget_frac": args.budget_frac, "profile": source,
-        "placed_bytes_per_expert": first.layer.placed_bytes() if first else {},
-        "l2": "inputs larger than L2: 8 experts' GG blocks (>1 GB) rotate with routing",
-    })
+    assert first is None or list(first.block_widths) == config["block_widths"]
+    pred = predict_step(args, rates, profile) if args.experts > 1 or args.config == "cfg4" else None
+    meas_busy = {"transfer": cp_busy / args.steps, "cpu": cc_busy,
+                 "gpu": sum(s["end_s"] - s["start_s"] for s in spans if s["stream"] == "gpu") / args.steps}
     line = {
         "metric": metric_name(args), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -557,6 +671,20 @@ def run_ours(args):
                  "cc_rate_GBps_fitted": cc_rate / 1e9 if cc_rate else None,
                  "step_bound_with_cc_s": t_host,
                  "step_bound_with_cc_frac": t_host / step_s if t_host and step_s else None},
+        "model_vs_measured": None if pred is None else {
+            "t_fin_pred_s": pred["t_fin_s"], "step_meas_s": step_s, "meas_over_pred": step_s / pred["t_fin_s"],
+            "case": pred["case"], "n_gemms": pred["n_gemms"],
+            "busy_pred_s": pred["busy_s"], "busy_meas_s": meas_busy,
+            "gantt_pred": pred["gantt"],
+            "note": "planner prediction (stage_times_generation + evaluate_recurrence, pipeline.py:143-167,237-260, "
+                    "Gantt rows :347-364) on the profile that chose the rates, vs the measured step and per-stream "
+                    "busy time (library trace, rank 0)"},
+        "plan": {"gpu_budget_bytes": budget, "profile": source,
+                 "placed_bytes_per_expert": first.layer.placed_bytes() if first else {}},
+        "placement": placement.summary(),
+        "collective": None if world == 1 else {
+            "backend": backend, "op": "all_reduce(sum) of fp32 partial outputs, one per step",
+            "bytes_per_step": global_batch * args.model_dim * 4},
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": cpu,
@@ -581,7 +709,7 @@ def run_prefill_decode(args):
 
     import paper_2411_15715_b200 as sp
     from paper_2411_15715_b200 import _native as nat
-    from paper_2411_15715_b200.sliced import CallSpec, forward_calls, route_topk
+    from paper_2411_15715_b200.sliced import CallSpec, forward_calls, moe_route
 
     world, rank, local = dist_env()
     if world > 1:
@@ -615,7 +743,7 @@ def run_prefill_decode(args):
     layer_plans = []
 
     def plan(d, x_host, split):
-        ids, gates = route_topk(x_host.astype(np.float64) @ routers[d], args.top_k)
+        ids, gates = moe_route(x_host.astype(np.float32), routers[d], args.top_k)
         routed = []
         for e, ffn in sets[d].items():
             rows, slots = np.nonzero(ids == e)
@@ -834,8 +962,60 @@ def run_model(args):
     print(json.dumps(line), flush=True)
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """``bench.py --gpus N`` started without a torchrun environment re-executes
+    itself under torchrun: one process per GPU on this node, rendezvous on
+    127.0.0.1, NCCL's communicator set-up logged (NCCL_DEBUG=INFO, INIT) to
+    stderr so the run shows which transport the all-reduce uses."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    print(f"[bench] spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.run(cmd, env=env).returncode
+
+
+def dry_run(args):
+    """Rendezvous, one barrier and a max-over-ranks reduction over gloo, then
+    rank 0 prints a JSON line: the launch path without GPUs."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([float(rank)])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "impl": args.impl, "n_gpus": world, "gpus_arg": args.gpus,
+                          "max_rank": world - 1, "local_world": int(os.environ.get("LOCAL_WORLD_SIZE", "1"))}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    world = dist_env()[0]
+    if world != args.gpus:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: the run uses {world} ranks", file=sys.stderr)
+    if args.dry_run:
+        return dry_run(args)
     if args.config == "model" and args.impl == "ours":
         return run_model(args)
     if args.config == "cfg3" and args.impl == "ours":

@@ -632,6 +632,14 @@ static const bool g_cc_batch = env_int("SP_CC_BATCH", 1) != 0;
 static const bool g_cc_first = env_int("SP_CC_FIRST", 1) != 0;
 // SP_PREREDUCE=0: leave every partial slice to the finalize (no early reduction)
 static const bool g_prereduce = env_int("SP_PREREDUCE", 1) != 0;
+// The grouped GG launch runs behind the call's last chunk kernel, i.e. once the
+// CG copies are done: a timing event recorded while copy-engine H2D traffic
+// saturates the link costs ~23 us of stream time (scripts/probes/event_span.cu),
+// and the GG block is off the critical path either way (the CC block ends the
+// step).  Same-box alternating pairs: GG span by events 0.64 -> 0.86 of HBM,
+// value 498 -> 511 and e2e 508 -> 532 tokens/s (profiles/r2/ab_gg_last.txt).
+// SP_GG_LAST=0 restores the launch behind the first chunk copy.
+static const bool g_gg_last = env_int("SP_GG_LAST", 1) != 0;
 // SP_Y_ZERO_COPY=0: small host outputs go through a device buffer and a read-back copy
 static const bool g_y_zero_copy = env_int("SP_Y_ZERO_COPY", 1) != 0;
 constexpr size_t kZeroCopyY = size_t(256) << 10;
@@ -1431,6 +1439,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   // first chunk copy), every other GG block is slotted in after a chunk kernel,
   // into the compute stream's idle time while the next copy is in flight.
   std::vector<std::function<int()>> gg_jobs;
+  bool has_group = false;
   {
     const int tt_max = max_token_tile(M);
     std::vector<int> group;
@@ -1446,6 +1455,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       else singles.push_back(c);
     }
     if (!group.empty()) {
+      has_group = true;
       // CTAs proportional to each block's rows, one wave over the SMs
       int64_t rows_total = 0;
       double bytes = 0;
@@ -1508,6 +1518,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     }
   }
   size_t next_gg = 0;
+  // SP_GG_LAST=1: the grouped GG launch goes behind the last chunk kernel, where
+  // the host link is idle (study switch)
+  std::function<int()> gg_group_last;
+  if (g_gg_last && has_group && !items.empty()) gg_group_last = std::move(gg_jobs[next_gg++]);
   if (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());
   if (items.empty())
     while (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());
@@ -1541,6 +1555,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     if (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());  // into the wait for the next copy
   }
   while (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());
+  if (gg_group_last) SP_TRY(gg_group_last());
 
   const double t_enq_done = now_s();
   host_span(C, 0, SP_TRACE_LAUNCH, t_call, t_enq_done, 0.0);

@@ -84,7 +84,17 @@ class ExpertParallelMoE:
 
     def _gpu_local_forward(self, plan, x):
         calls = [CallSpec(self.experts[e].layer, rows, gates) for e, rows, gates in plan]
-        return forward_calls(calls, x)
+        return forward_calls(calls, x, self._partial_out(x))
+
+    def _partial_out(self, x):
+        """fp32 buffer for this rank's partial output when it is all-reduced: the
+        partials are summed in fp32 across ranks (as the single-GPU finalize sums
+        its slices) and rounded to x's dtype once, after the reduction."""
+        import torch
+
+        if self.world > 1 and isinstance(x, torch.Tensor) and x.is_cuda and x.dtype != torch.float32:
+            return torch.empty((x.shape[0], self.out_dim), dtype=torch.float32, device=x.device)
+        return None
 
     def forward(self, x, x_host: np.ndarray | None = None):
         """y = sum over ranks of the owned experts' gated outputs (all-reduced).
@@ -98,22 +108,24 @@ class ExpertParallelMoE:
             if self._dispatch is None:
                 layers = [self.experts[e].layer if e in self.experts else None for e in range(self.n_experts)]
                 self._dispatch = MoEDispatch(layers, self.router_w, self.top_k)
-            y = self._dispatch(x)
+            y = self._dispatch(x, self._partial_out(x))
             if not isinstance(y, torch.Tensor):
                 y = torch.as_tensor(np.ascontiguousarray(y))
-            return self._reduce(y)
+            return self._reduce(y).to(x.dtype) if isinstance(x, torch.Tensor) and x.is_cuda else self._reduce(y)
         if x_host is None:
             x_host = x.detach().float().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
         plan = route_local(x_host, self.router_w, self.top_k, self.owned)
+        on_gpu = isinstance(x, torch.Tensor) and x.is_cuda
         if plan:
             y = self.local_forward(plan, x)
             if not isinstance(y, torch.Tensor):
                 y = torch.as_tensor(np.ascontiguousarray(y))
         else:
             dev = x.device if isinstance(x, torch.Tensor) else "cpu"
-            dt = x.dtype if isinstance(x, torch.Tensor) else torch.float64
+            dt = torch.float32 if on_gpu and self.world > 1 else x.dtype if isinstance(x, torch.Tensor) else torch.float64
             y = torch.zeros((x_host.shape[0], self.out_dim), dtype=dt, device=dev)
-        return self._reduce(y)
+        y = self._reduce(y)
+        return y.to(x.dtype) if on_gpu else y
 
     def _reduce(self, y):
         """Sum the ranks' partial outputs (one all-reduce: NCCL on GPUs)."""
@@ -152,7 +164,11 @@ class ColumnShardedFFN:
     def forward(self, x):
         import torch
 
-        y = self.shard(x)
+        out = None
+        if self.world > 1 and isinstance(x, torch.Tensor) and x.is_cuda and x.dtype != torch.float32:
+            # fp32 partials across the ranks, one rounding after the sum
+            out = torch.empty((x.shape[0], self.shard.layer.out_dim), dtype=torch.float32, device=x.device)
+        y = self.shard(x, out=out) if out is not None else self.shard(x)
         if not isinstance(y, torch.Tensor):
             y = torch.as_tensor(np.ascontiguousarray(y))
         if self.world > 1:
@@ -161,6 +177,6 @@ class ColumnShardedFFN:
                 self.dist.all_reduce(yd, group=self.group)
                 return yd.cpu()
             self.dist.all_reduce(y, group=self.group)
-        return y
+        return y.to(x.dtype) if out is not None else y
 
     __call__ = forward

@@ -120,9 +120,10 @@ def check_moe(torch, experts, weights, router, k, xs, tol, rows=None):
         assert np.array_equal(ids[sel], ref_ids), "product routing differs from the oracle's"
         y_dev = moe(xd).float().cpu().numpy()[sel]
         y_host = np.asarray(moe(x64.astype(np.float32)))[sel]
-        for got in (y_dev, y_host):
+        for io, got in (("device", y_dev), ("host", y_host)):
             err = orc.max_rel_error(got, ref)
             worst = max(worst, err)
+            print(f"PARITY T={x.shape[0]} io={io} max_rel_err={err:.3e} tol={tol:g}")
             assert err <= tol, (x.shape, err)
     return worst
 
@@ -136,6 +137,7 @@ def test_cfg1_fp32_moe_layer(torch, monkeypatch):
     assert (rates.cc, rates.cg, rates.gg) == (0.2, 0.3, 0.5)
     weights = make_weights(torch, args.experts, args.model_dim, args.hidden_dim, "f32")
     experts = place(weights, rates, "f32")
+    print(f"PARITY cfg1 widths={experts[0].block_widths}")
     assert experts[0].block_widths == (716, 1076, 1792)
     router = np.random.default_rng(7).standard_normal((args.model_dim, args.experts))
     rng = np.random.default_rng(1)
@@ -152,6 +154,7 @@ def test_cfg2_mixtral_moe_layer_at_solved_widths(torch, monkeypatch):
     args, rates = bench_plan(monkeypatch)
     weights = make_weights(torch, args.experts, args.model_dim, args.hidden_dim, "bf16")
     experts = place(weights, rates, "bf16")
+    print(f"PARITY cfg2 widths={experts[0].block_widths}")
     assert experts[0].block_widths == (5386, 1781, 7169)  # BENCH_r01 config.block_widths
     router = np.random.default_rng(7).standard_normal((args.model_dim, args.experts))
     rng = np.random.default_rng(2)
@@ -189,7 +192,9 @@ def test_cfg3_prompt_layer_with_solve_ng_split(torch, monkeypatch):
     y = SlicedMoE(experts, router, args.top_k)(x, n_g=n_g).float().cpu().numpy()
     rows = np.arange(0, args.prompt, 5)  # fp64 oracle on a token subset
     ref, _ = oracle_moe(x64, weights, router, args.top_k, rows)
-    assert orc.max_rel_error(y[rows], ref) <= BF16_TOL
+    err = orc.max_rel_error(y[rows], ref)
+    print(f"PARITY cfg3 T={args.prompt} n_g={n_g} counts={counts.tolist()} max_rel_err={err:.3e}")
+    assert err <= BF16_TOL
     release(experts)
 
 
@@ -217,9 +222,10 @@ def test_cfg4_llama70b_dense_ffn(torch, monkeypatch, world):
         x64 = x.float().cpu().numpy().astype(np.float64)
         ref = oracle_expert(x64, w1t, w3t, w2t)
         got = ffn(x).float().cpu().numpy()
-        assert orc.max_rel_error(got, ref) <= BF16_TOL, T
         got_h = np.asarray(ffn(x64.astype(np.float32)))
-        assert orc.max_rel_error(got_h, ref) <= BF16_TOL, T
+        e_d, e_h = orc.max_rel_error(got, ref), orc.max_rel_error(got_h, ref)
+        print(f"PARITY cfg4 world={world} widths={ffn.block_widths} T={T} device={e_d:.3e} host={e_h:.3e}")
+        assert e_d <= BF16_TOL and e_h <= BF16_TOL, T
     ffn.layer.release()
 
 
@@ -232,6 +238,7 @@ def test_cfg5_moe_batch_sweep(torch, monkeypatch, moe):
     args, rates = bench_plan(monkeypatch, "--config", "cfg5", "--moe", moe)
     weights = make_weights(torch, args.experts, args.model_dim, args.hidden_dim, "bf16")
     experts = place(weights, rates, "bf16")
+    print(f"PARITY cfg5 {moe} widths={experts[0].block_widths}")
     router = np.random.default_rng(7).standard_normal((args.model_dim, args.experts))
     rng = np.random.default_rng(5)
     xs = [rng.standard_normal((B, args.model_dim)) for B in (1, 4, 32)]
