@@ -84,6 +84,9 @@ def parse(argv=None):
                     help="spawn / rendezvous / barrier only (CPU test of the multi-rank launch path)")
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--calibrate", type=int, default=1,
+                    help="rescale the profile's host CPU / link terms from traced steps on this box and re-solve")
+    ap.add_argument("--calib-steps", type=int, default=16)
     args = ap.parse_args(argv)
     if args.config == "cfg1":
         args.model_dim, args.hidden_dim, args.dtype = 1024, 3584, "f32"
@@ -211,12 +214,22 @@ def plan_rates(args, tokens_per_step):
     budget = args.budget_frac * layer.layer_bytes
     if args.config == "cfg1":
         return sp.SlicingRates(0.2, 0.3, 0.5), budget, "fixed 0.2/0.3/0.5 (BASELINE configs[0])", profile
+    rates = solve_rates(args, profile, budget)
+    if getattr(args, "force_cc", -1.0) >= 0.0:
+        source += f" (r_CC forced to {args.force_cc}: probe, not the planner's split)"
+    return rates, budget, source, profile
+
+
+def solve_rates(args, profile, budget):
+    """greedy_assign (memory_assigner.py:37-122) then solve_rcg (rate_solver.py:90-117)."""
+    import paper_2411_15715_b200 as sp
+
+    layer, wl = args.plan_layer, args.plan_workload
     mem = sp.greedy_assign(profile, [layer], wl, budget, n_steps=16)
     rates = sp.solve_rcg(profile, layer, wl, mem.per_layer_rgg[0]).rates
     if getattr(args, "force_cc", -1.0) >= 0.0:
         rates = sp.SlicingRates(args.force_cc, 1.0 - rates.gg - args.force_cc, rates.gg)
-        source += f" (r_CC forced to {args.force_cc}: probe, not the planner's split)"
-    return rates, budget, source, profile
+    return rates
 
 
 def predict_step(args, rates, profile) -> dict:
@@ -233,6 +246,39 @@ def predict_step(args, rates, profile) -> dict:
             "busy_s": {"transfer": stage.transfer_s * layer.n_gemms, "gpu": stage.gpu_s * layer.n_gemms,
                        "cpu": stage.cpu_s * layer.n_gemms, "launch": stage.launch_s * layer.n_gemms},
             "gantt": sp.timeline_records(stage, tl)}
+
+
+def calibrate_host_terms(args, profile, rates, spans, steps) -> tuple:
+    """Per-box recalibration of the host side of the cost model.
+
+    The committed profile was fitted on one pool box; host DRAM bandwidth (the
+    CC block) and the effective link rate under that load (the CG copies) vary
+    box to box.  ``spans`` are the library trace of ``steps`` real decode steps
+    at ``rates``: the measured CC busy time and copy busy time per step are
+    divided by what the profile predicts for the same step
+    (stage_times_generation, pipeline.py:143-167), and the profile's CPU GEMM
+    and PCIe terms (alpha and beta) are scaled by those ratios -- the same
+    linear model (perf_model.py:99-128), re-anchored on this box.  The caller
+    re-runs solve_rcg on the result."""
+    from paper_2411_15715_b200 import costs
+
+    pred = predict_step(args, rates, profile)["busy_s"]
+    meas_cpu = sum(s["end_s"] - s["start_s"] for s in spans if s["kind"] == "cc") / steps
+    meas_link = sum(s["end_s"] - s["start_s"] for s in spans if s["kind"] == "copy") / steps
+    k_cpu = meas_cpu / pred["cpu"] if pred["cpu"] > 0 and meas_cpu > 0 else 1.0
+    k_link = meas_link / pred["transfer"] if pred["transfer"] > 0 and meas_link > 0 else 1.0
+    doc = costs.profile_to_dict(profile)
+    for g in doc.get("gemm", {}).values():
+        if "cpu" in g:
+            g["cpu"]["alpha"] *= k_cpu
+            g["cpu"]["beta"] *= k_cpu
+    if "pcie" in doc:
+        doc["pcie"]["alpha"] *= k_link
+        doc["pcie"]["beta"] *= k_link
+    info = {"k_cpu": k_cpu, "k_link": k_link, "steps": steps,
+            "cpu_busy_s": {"measured": meas_cpu, "predicted": pred["cpu"]},
+            "transfer_busy_s": {"measured": meas_link, "predicted": pred["transfer"]}}
+    return costs.profile_from_dict(doc), info
 
 
 # ---------------------------------------------------------------------------
@@ -410,22 +456,21 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def base_config(args, rates, global_batch, world):
+def base_config(args, global_batch, world):
     """The config both arms print (identical dicts, so the driver's same-config
-    check compares like with like)."""
-    from paper_2411_15715_b200.sliced import split_boundaries
+    check compares like with like).  The split the GPU arm executes (rates,
+    block widths) is reported under its own ``split`` key: it is re-planned on
+    each box, and the reference arm's fp64 forward computes all three blocks on
+    the host whatever the split."""
 
     wl = {"cfg1": "cfg1-1024x3584-moe-ffn-decode", "cfg2": "mixtral-8x7b-moe-ffn-decode",
           "cfg4": "llama2-70b-dense-ffn-decode-colsharded",
           "cfg5": f"{'phimoe' if args.moe == 'phimoe' else 'mixtral-8x22b'}-moe-ffn-decode-ep"}.get(args.config, args.config)
-    hidden = getattr(args, "shard_hidden", args.hidden_dim)
-    b1, b2 = split_boundaries(hidden, rates)
     return {"workload": wl,
             "model_dim": args.model_dim, "hidden_dim": args.hidden_dim, "experts": args.experts,
             "top_k": args.top_k, "batch_per_gpu": args.batch, "global_batch": global_batch,
             "parallelism": (f"col{world}" if args.config == "cfg4" else f"ep{world}") if world > 1 else "single",
-            "rates": {"cc": rates.cc, "cg": rates.cg, "gg": rates.gg},
-            "block_widths": [b1, b2 - b1, hidden - b2], "budget_frac": args.budget_frac,
+            "budget_frac": args.budget_frac,
             "l2": "inputs larger than L2: the experts' GG blocks (>1 GB) rotate with routing"}
 
 
@@ -457,7 +502,7 @@ def run_reference(args):
         "impl": "reference", "metric": metric_name(args), "value": r["value"], "unit": UNIT, "n_gpus": world,
         "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["s_per_step"] * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": base_config(args, rates, global_batch, world),
+        "config": base_config(args, global_batch, world),
         "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["threads"], "kind": "port",
                          "sample": r["sample"], "best": r["best"], "median": r["median"], "threadpool": r["threadpool"]},
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -523,6 +568,7 @@ def run_ours(args):
         lo, hi = column_shard(args.hidden_dim, rank, world)
         args.shard_hidden = hi - lo
     rates, budget, source, profile = plan_rates(args, B)
+    fitted = profile  # the committed fit: link peak and in-situ CC rate for the roofline keys
     rng = np.random.default_rng(7)
     if args.config == "cfg4":
         experts = make_experts(args, rates, [rank], device, hidden=hi - lo)
@@ -549,7 +595,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         if trace:
-            nat.trace_enable(True)
+            nat.trace_enable(True, gg_only=(trace == "gg"))
         l0 = nat.stats()["kernel_launches"]
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -578,17 +624,56 @@ def run_ours(args):
         step(i, host_io=True)
     torch.cuda.synchronize()
 
+    # ---- per-box recalibration of the host terms, then re-plan (before timing) ----
+    calib = None
+    if args.calibrate and args.config != "cfg1" and (args.experts > 1 or args.config == "cfg4"):
+        t_cal = time.perf_counter()
+        rates0, profile0 = rates, profile
+        _, _, _, cspans = timed(args.calib_steps, trace="full")
+        profile, calib = calibrate_host_terms(args, profile, rates, cspans, args.calib_steps)
+        rates = solve_rates(args, profile, budget)
+        source += f" (host terms recalibrated on this box: CPU x{calib['k_cpu']:.3f}, link x{calib['k_link']:.3f})"
+        from dataclasses import asdict
+
+        from paper_2411_15715_b200.sliced import split_boundaries
+
+        t_fin0 = predict_step(args, rates0, profile0)["t_fin_s"]
+        resliced = False
+        w0 = next(iter(experts.values())).block_widths if experts else None
+        if experts and tuple(split_boundaries(w0[0] + w0[1] + w0[2], rates)) != (w0[0], w0[0] + w0[1]):
+            new_experts = {e: ex.reslice(rates) for e, ex in experts.items()}
+            for ex in experts.values():
+                ex.layer.release()
+            experts = new_experts
+            resliced = True
+            if args.config == "cfg4":
+                moe = ColumnShardedFFN(experts[rank])
+            else:
+                moe = ExpertParallelMoE(experts, router, args.top_k, args.experts, out_dim=args.model_dim)
+            for i in range(args.warmup):
+                step(i)
+                step(i, host_io=True)
+            torch.cuda.synchronize()
+        calib.update({"rates_before": asdict(rates0), "rates_after": asdict(rates), "resliced": resliced,
+                      "t_fin_pred_before_s": t_fin0, "seconds": time.perf_counter() - t_cal})
+
     clk = ClockSampler(local).start()
     clk.armed = True
-    ms_step, wall_step, launches, spans = timed(args.steps, trace=True)
+    # the headline region records device events only around the GG launches (the
+    # roofline kernel) plus host-clock CC spans: full tracing puts events on the
+    # saturated copy stream and slows the step it measures
+    ms_step, wall_step, launches, gg_spans = timed(args.steps, trace="gg")
     clk.armed = False
     clk.stop()
     clocks = clk.summary()
     # SP_BENCH_TRACE_E2E=path: also trace the e2e region (probe; the e2e number then carries the trace cost)
     e2e_trace = os.environ.get("SP_BENCH_TRACE_E2E", "")
-    e2e_ms, _, _, e2e_spans = timed(args.steps, host_io=True, trace=bool(e2e_trace))
+    e2e_ms, _, _, e2e_spans = timed(args.steps, host_io=True, trace="full" if e2e_trace else False)
     if e2e_trace and rank == 0:
         Path(e2e_trace).write_text(json.dumps(e2e_spans))
+    # a third region of the same steps, fully traced: per-stream busy time, copy
+    # rates and the measured Gantt (analysis only; its own step time is reported)
+    full_ms, _, _, spans = timed(args.steps, trace="full")
     value = global_batch / (ms_step * 1e-3)
     e2e_value = global_batch / (e2e_ms * 1e-3)
 
@@ -596,7 +681,7 @@ def run_ours(args):
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"
-    gg = [s for s in spans if s["kind"] == "gg"]
+    gg = [s for s in gg_spans if s["kind"] == "gg"]
     cp = [s for s in spans if s["kind"] == "copy"]
     cc = [s for s in spans if s["kind"] == "cc"]
     gg_bytes = float(np.mean([s["bytes"] for s in gg])) if gg else 0.0
@@ -610,15 +695,15 @@ def run_ours(args):
     gg_dev_dt = float(np.mean(gg_dev)) if gg_dev else 0.0
     cp_bytes = sum(s["bytes"] for s in cp)
     cp_busy = sum(s["end_s"] - s["start_s"] for s in cp)
-    link_peak = 1.0 / profile.pcie.beta / 1e9 if profile.pcie and profile.pcie.beta else 55.5
+    link_peak = 1.0 / fitted.pcie.beta / 1e9 if fitted.pcie and fitted.pcie.beta else 55.5
     step_s = ms_step * 1e-3
-    gg_step_bytes = sum(s["bytes"] for s in gg) / args.steps
+    gg_step_bytes = sum(s["bytes"] for s in spans if s["kind"] == "gg") / args.steps
     cg_step_bytes = cp_bytes / args.steps
     t_roof = max(gg_step_bytes / (hbm_peak * 1e9), cg_step_bytes / (link_peak * 1e9))
     cc_busy = sum(s["end_s"] - s["start_s"] for s in cc) / args.steps
     # the host side of the step: CC bytes at the profile's fitted (in-situ) CC rate
     cc_step_bytes = sum(s["bytes"] for s in cc) / args.steps
-    g16 = profile.gemm.get(sp_precision_fp16()) if profile.gemm else None
+    g16 = fitted.gemm.get(sp_precision_fp16()) if fitted.gemm else None
     cc_rate = 2.0 / g16.cpu.beta if g16 is not None and g16.cpu and g16.cpu.beta else None
     t_host = max(t_roof, cc_step_bytes / cc_rate) if cc_rate else None
     if args.trace_out and rank == 0:
@@ -642,8 +727,13 @@ def run_ours(args):
 
     first = next(iter(experts.values())) if experts else None
     xel = 2 if args.dtype == "bf16" else 4
-    config = base_config(args, rates, global_batch, world)
-    assert first is None or list(first.block_widths) == config["block_widths"]
+    from paper_2411_15715_b200.sliced import split_boundaries
+
+    config = base_config(args, global_batch, world)
+    hidden = getattr(args, "shard_hidden", args.hidden_dim)
+    b1, b2 = split_boundaries(hidden, rates)
+    split = {"rates": {"cc": rates.cc, "cg": rates.cg, "gg": rates.gg}, "block_widths": [b1, b2 - b1, hidden - b2]}
+    assert first is None or list(first.block_widths) == split["block_widths"]
     pred = predict_step(args, rates, profile) if args.experts > 1 or args.config == "cfg4" else None
     meas_busy = {"transfer": cp_busy / args.steps, "cpu": cc_busy,
                  "gpu": sum(s["end_s"] - s["start_s"] for s in spans if s["stream"] == "gpu") / args.steps}
@@ -652,6 +742,8 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (random-init weights, seeded)",
         "config": config,
+        "split": split,
+        "calibration": calib,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": global_batch * args.model_dim * xel,
                 "d2h_bytes_per_step": global_batch * args.model_dim * 4},
         "roofline": {"bound": "hbm", "kernel": "ffn_block_kernel on the GG block (fused up+gate+down, TMA bulk ring)",
@@ -676,9 +768,11 @@ def run_ours(args):
             "case": pred["case"], "n_gemms": pred["n_gemms"],
             "busy_pred_s": pred["busy_s"], "busy_meas_s": meas_busy,
             "gantt_pred": pred["gantt"],
+            "step_full_trace_s": full_ms * 1e-3,
             "note": "planner prediction (stage_times_generation + evaluate_recurrence, pipeline.py:143-167,237-260, "
                     "Gantt rows :347-364) on the profile that chose the rates, vs the measured step and per-stream "
-                    "busy time (library trace, rank 0)"},
+                    "busy time (library trace of a separate, fully traced region of the same steps, rank 0; "
+                    "step_full_trace_s is that region's own step time)"},
         "plan": {"gpu_budget_bytes": budget, "profile": source,
                  "placed_bytes_per_expert": first.layer.placed_bytes() if first else {}},
         "placement": placement.summary(),

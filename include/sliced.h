@@ -197,7 +197,9 @@ typedef struct sp_trace_record {
                    * copy engine saturates the host link.                 */
 } sp_trace_record;
 /* on != 0 clears the trace and starts recording (events on the library's own
- * streams, host clock for CC); sp_trace_fetch synchronises the device. */
+ * streams, host clock for CC); on == 2 records GPU spans only around GG
+ * launches (plus every host span), which leaves the step's timing untouched;
+ * sp_trace_fetch synchronises the device. */
 int sp_trace_enable(int on);
 int sp_trace_fetch(sp_trace_record* out, int* n);
 /* Kernels launched and bytes copied host-to-device by the library so far. */

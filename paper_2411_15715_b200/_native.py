@@ -172,8 +172,10 @@ def _default_device() -> int:
     return 0
 
 
-def trace_enable(on: bool = True) -> None:
-    check(lib().sp_trace_enable(1 if on else 0))
+def trace_enable(on: bool = True, gg_only: bool = False) -> None:
+    """``gg_only``: device spans only around GG launches (plus host spans), so
+    the traced region keeps the timing of an untraced one."""
+    check(lib().sp_trace_enable((2 if gg_only else 1) if on else 0))
 
 
 def trace_fetch() -> list[dict]:

@@ -151,6 +151,12 @@ struct Span {
 };
 struct Trace {
   bool on = false;
+  // sp_trace_enable(2): GPU spans only around GG launches (the roofline
+  // kernel); copy / chunk / merge spans are skipped, so the traced step keeps
+  // the timing of an untraced one (events on the copy stream cost stream time
+  // while the link is saturated, scripts/probes/event_span.cu).  Host spans
+  // are always recorded (host clock, no device work).
+  bool gg_only = false;
   cudaEvent_t t0 = nullptr;
   double host_t0 = 0;
   int call = 0;
@@ -945,7 +951,7 @@ struct GpuSpan {
   Span sp;
   bool on;
   GpuSpan(Context* c, cudaStream_t st, int stream, int kind, double bytes)
-      : C(c), s(st), on(c->trace.on) {
+      : C(c), s(st), on(c->trace.on && (!c->trace.gg_only || kind == SP_TRACE_GG)) {
     if (!on) return;
     sp.stream = stream;
     sp.kind = kind;
@@ -2200,6 +2206,7 @@ int sp_trace_enable(int on) {
   tr.spans.clear();
   tr.call = 0;
   tr.on = on != 0;
+  tr.gg_only = on == 2;
   tr.kspan_next = 0;
   tr.kslot_cur = -1;
   if (tr.on) {

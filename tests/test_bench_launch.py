@@ -34,15 +34,17 @@ def test_reference_arm_times_the_global_batch_at_n_ranks():
     assert line["impl"] == "reference" and line["n_gpus"] == 2
     cfg = line["config"]
     assert cfg["global_batch"] == 2 and cfg["batch_per_gpu"] == 1 and cfg["parallelism"] == "ep2"
-    assert cfg["block_widths"] == [716, 1076, 1792]
+    assert "block_widths" not in cfg and "rates" not in cfg  # the executed split is the GPU arm's `split` key
+    assert "cc=0.2000 cg=0.3000 gg=0.5000" in line["cpu_baseline"]["sample"]
     assert "2 token(s)" in line["cpu_baseline"]["sample"]
     assert line["cpu_baseline"]["best"] >= line["cpu_baseline"]["median"] > 0
     assert line["cpu_baseline"]["threadpool"]
 
 
 def test_both_arms_share_one_config_builder():
-    """run_ours prints base_config(...) unchanged (extra planning detail goes
-    under `plan`), so the two arms' config dicts have the same keys and values."""
+    """run_ours prints base_config(...) unchanged (the executed split goes under
+    `split`, planning detail under `plan` / `calibration`), so the two arms'
+    config dicts have the same keys and values."""
     src = (ROOT / "bench.py").read_text()
-    assert "config = base_config(args, rates, global_batch, world)" in src
+    assert "config = base_config(args, global_batch, world)" in src
     assert "config.update(" not in src
