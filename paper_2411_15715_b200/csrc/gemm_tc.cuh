@@ -71,6 +71,15 @@ struct GemmArgs {
   int dbg_no_mma;  // probe: stream the operands but issue no MMA (SP_TC_DBG_NOMMA)
 };
 
+// Programmatic dependent launch (PDL).  The prefill chain gather -> up GEMM ->
+// (swiglu_reduce) -> down GEMM is launched with programmatic stream
+// serialization: each kernel lets its successor launch early and the successor
+// streams the operands that do not depend on its predecessor (the weights)
+// before it waits.  Launched without the attribute, both are no-ops.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -181,14 +190,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  const int nk = kb1 - kb0;
+  grid_dep_launch();  // the successor may start its weight stream on the SMs this grid leaves idle
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const int i = kb - kb0, s = i % S;
-        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+      auto load_a = [&](int i) {
+        const int kb = kb0 + i, s = i % S;
         unsigned char* st = smem + size_t(s) * STAGE;
-        mbar_expect_tx(&full[s], STAGE);
         if constexpr (!DOWN) {
           tma_load_2d(st, &tmA0, &full[s], kb * BK, m0);
           if constexpr (NA == 2) tma_load_2d(st + A_BYTES, &tmA1, &full[s], kb * BK, m0);
@@ -200,14 +209,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(st + a * A_BYTES + BK * 128, &tmA0, &full[s], m0 + a * BM + 64, kb * BK);
           }
         }
-        tma_load_2d(st + NA * A_BYTES, &tmB, &full[s], kb * BK, t0);
+      };
+      auto load_b = [&](int i) {
+        const int kb = kb0 + i, s = i % S;
+        tma_load_2d(smem + size_t(s) * STAGE + NA * A_BYTES, &tmB, &full[s], kb * BK, t0);
+      };
+      // the first S stages' weights do not depend on the predecessor kernel:
+      // issue them before waiting for it, then the dependent x / a tiles
+      const int pre = nk < S ? nk : S;
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(&full[i], STAGE);
+        load_a(i);
+      }
+      grid_dep_wait();
+      for (int i = 0; i < pre; ++i) load_b(i);
+      for (int i = pre; i < nk; ++i) {
+        const int s = i % S;
+        mbar_wait(&empty[s], ((i / S) - 1) & 1);
+        mbar_expect_tx(&full[s], STAGE);
+        load_a(i);
+        load_b(i);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = umma_idesc(BM, NT, a_mn);
-    for (int kb = kb0; kb < kb1; ++kb) {
-      const int i = kb - kb0, s = i % S;
+    for (int i = 0; i < nk; ++i) {
+      const int s = i % S;
       mbar_wait(&full[s], (i / S) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (lane == 0) {
@@ -225,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         umma_commit(&empty[s]);  // the probe still hands every stage back
-        if (kb == kb1 - 1) umma_commit(tmem_full);
+        if (i == nk - 1) umma_commit(tmem_full);
       }
       __syncwarp();
     }
@@ -237,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16);
     const int et = threadIdx.x - 64;      // 0..127
     float* part = g.partial + (size_t(tile) * g.ks + ks_id) * NA * NT * BM;
+    grid_dep_wait();  // outputs are written only once the predecessor grid is complete
     if (kb1 > kb0) {
       mbar_wait(tmem_full, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -502,26 +531,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  const int nk = kb1 - kb0;
+  grid_dep_launch();
   if (warp == 0) {
     // ---------------- TMA producer (both ranks) ----------------
     if (lane == 0) {
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const int i = kb - kb0, s = i % S;
-        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+      auto load_a = [&](int i) {
+        const int kb = kb0 + i, s = i % S;
         unsigned char* st = smem + size_t(s) * STAGE;
         const uint32_t lbar = map_to_rank(&full[s], 0);
-        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE);
         tma_load_2d_pair(st, &tmA0, lbar, kb * BK, m0);
         if constexpr (NA == 2) tma_load_2d_pair(st + A_BYTES, &tmA1, lbar, kb * BK, m0);
-        tma_load_2d_pair(st + NA * A_BYTES, &tmB, lbar, kb * BK, t0 + int(rank) * HALF);
+      };
+      auto load_b = [&](int i) {
+        const int kb = kb0 + i, s = i % S;
+        tma_load_2d_pair(smem + size_t(s) * STAGE + NA * A_BYTES, &tmB, map_to_rank(&full[s], 0), kb * BK,
+                         t0 + int(rank) * HALF);
+      };
+      const int pre = nk < S ? nk : S;
+      for (int i = 0; i < pre; ++i) {
+        if (rank == 0) mbar_expect_tx(&full[i], 2 * STAGE);
+        load_a(i);
+      }
+      grid_dep_wait();
+      for (int i = 0; i < pre; ++i) load_b(i);
+      for (int i = pre; i < nk; ++i) {
+        const int s = i % S;
+        mbar_wait(&empty[s], ((i / S) - 1) & 1);
+        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE);
+        load_a(i);
+        load_b(i);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (rank 0 only) ----------------
     if (rank == 0) {
       const uint32_t idesc = umma_idesc(2 * BM, NT, false);
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const int i = kb - kb0, s = i % S;
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % S;
         mbar_wait(&full[s], (i / S) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
@@ -535,7 +582,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                              (i > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit_pair(&empty[s]);
-          if (kb == kb1 - 1) umma_commit_pair(tmem_full);
+          if (i == nk - 1) umma_commit_pair(tmem_full);
         }
         __syncwarp();
       }
@@ -546,6 +593,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int row = quarter * 32 + lane;
     const int m = m0 + row;
     const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16);
+    grid_dep_wait();
     if (kb1 > kb0) {
       mbar_wait(tmem_full, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -590,6 +638,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // a[t, h] = act(sum_q z[q][0][t][h]) [* sum_q z[q][1][t][h]], splits summed in order
 __global__ void swiglu_reduce_kernel(const float* __restrict__ z, int ks, int na, int T, int R, int64_t zld,
                                      int act, __nv_bfloat16* __restrict__ a_out, int64_t lda) {
+  grid_dep_launch();
+  grid_dep_wait();  // z comes from the up GEMM
   const int t = blockIdx.y;
   const int h = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (h >= R) return;
@@ -612,12 +662,33 @@ __global__ void swiglu_reduce_kernel(const float* __restrict__ z, int ks, int na
   for (int e = 0; e < 4 && h + e < R; ++e) dst[e] = __float2bfloat16_rn(o[e]);
 }
 
-// gather x rows (any dtype) into a contiguous bf16 [T, ldo] buffer
+// gather x rows (any dtype) into a contiguous bf16 [T, ldo] buffer; `vec`: 8 elements
+// per thread with 16-byte (bf16) / 2 x 16-byte (f32) loads (rows 16-byte aligned)
 __global__ void gather_rows_bf16_kernel(const void* x, int xdtype, int64_t ldx_in, const int32_t* ids, int t0,
-                                        int T, int M, __nv_bfloat16* out, int64_t ldo) {
+                                        int T, int M, __nv_bfloat16* out, int64_t ldo, int vec) {
+  grid_dep_launch();  // the up GEMM starts streaming its weights meanwhile
   const int t = blockIdx.y;
   if (t >= T) return;
   const int64_t row = ids ? ids[t0 + t] : int64_t(t0 + t);
+  if (vec) {
+    for (int k = (blockIdx.x * blockDim.x + threadIdx.x) * 8; k < M; k += gridDim.x * blockDim.x * 8) {
+      uint4 o;
+      if (xdtype == 1) {
+        o = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + row * ldx_in + k);
+      } else {
+        const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(x) + row * ldx_in + k);
+        const float4 a = src[0], b = src[1];
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(a.x, a.y), p1 = __floats2bfloat162_rn(a.z, a.w);
+        __nv_bfloat162 p2 = __floats2bfloat162_rn(b.x, b.y), p3 = __floats2bfloat162_rn(b.z, b.w);
+        o.x = *reinterpret_cast<uint32_t*>(&p0);
+        o.y = *reinterpret_cast<uint32_t*>(&p1);
+        o.z = *reinterpret_cast<uint32_t*>(&p2);
+        o.w = *reinterpret_cast<uint32_t*>(&p3);
+      }
+      *reinterpret_cast<uint4*>(out + int64_t(t) * ldo + k) = o;
+    }
+    return;
+  }
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < M; k += gridDim.x * blockDim.x) {
     const float v = xdtype == 1 ? bf16_to_f(static_cast<const uint16_t*>(x)[row * ldx_in + k])
                                 : static_cast<const float*>(x)[row * ldx_in + k];

@@ -683,9 +683,33 @@ static int make_tmap(CUtensorMap* map, const void* base, int64_t inner, int64_t 
   return SP_OK;
 }
 
+// SP_TC_PDL=0: the prefill chain's kernels wait for full completion of their predecessor
+static const bool g_tc_pdl = env_int("SP_TC_PDL", 1) != 0;
+
+// Launch with programmatic stream serialization when `pdl` (the kernel's
+// griddepcontrol.wait then orders it after its predecessor; everything it does
+// before that wait -- barrier init, TMEM alloc, the first weight stages --
+// overlaps the predecessor's tail).  Only used when the previous operation on
+// `s` is one of this chain's kernels.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (pdl && g_tc_pdl) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <int NT, int NA, bool DOWN>
 static int launch_gemm_t(Context* C, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
-                         tc::GemmArgs g, cudaStream_t s) {
+                         tc::GemmArgs g, cudaStream_t s, bool pdl) {
   auto kern = tc::gemm_kernel<NT, NA, DOWN>;
   constexpr int STAGE = NA * tc::BM * tc::BK * 2 + NT * tc::BK * 2;
   static bool attr_set = false;
@@ -702,7 +726,10 @@ static int launch_gemm_t(Context* C, const CUtensorMap& a0, const CUtensorMap& a
   const int budget = two_per_sm ? kSmemLimit / 2 - 1024 : kSmemLimit;
   g.stages = std::max(2, std::min(6, (budget - 1024 - 256) / STAGE));
   const size_t smem = size_t(g.stages) * STAGE + 1024 + 256;
-  if (g.ks > 1) {
+  if (g.ks > 1 && (DOWN ? !g.split_slices : !g.z)) {
+    // split-K fix-up through fp32 partial tiles (no current caller; allocating
+    // here puts stream operations inside the chain, so it never runs under PDL)
+    pdl = false;
     const size_t need = size_t(g.m_tiles) * g.t_tiles * g.ks * NA * NT * tc::BM * 4;
     SP_TRY(C->tc_partial.ensure(need, s));
     g.partial = static_cast<float*>(C->tc_partial.p);
@@ -715,22 +742,21 @@ static int launch_gemm_t(Context* C, const CUtensorMap& a0, const CUtensorMap& a
   }
   static const int dbg_no_mma = env_int("SP_TC_DBG_NOMMA", 0);
   g.dbg_no_mma = dbg_no_mma;
-  kern<<<ctas, tc::kThreads, smem, s>>>(a0, a1, b, g);
-  SP_CUDA(cudaGetLastError());
+  SP_CUDA(launch_k(kern, dim3(ctas), dim3(tc::kThreads), smem, s, pdl, a0, a1, b, g));
   ++C->launches;
   return SP_OK;
 }
 
 template <int NA, bool DOWN>
 static int launch_gemm(Context* C, int nt, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
-                       const tc::GemmArgs& g, cudaStream_t s) {
+                       const tc::GemmArgs& g, cudaStream_t s, bool pdl) {
   switch (nt) {
-    case 16: return launch_gemm_t<16, NA, DOWN>(C, a0, a1, b, g, s);
-    case 32: return launch_gemm_t<32, NA, DOWN>(C, a0, a1, b, g, s);
-    case 64: return launch_gemm_t<64, NA, DOWN>(C, a0, a1, b, g, s);
-    case 128: return launch_gemm_t<128, NA, DOWN>(C, a0, a1, b, g, s);
+    case 16: return launch_gemm_t<16, NA, DOWN>(C, a0, a1, b, g, s, pdl);
+    case 32: return launch_gemm_t<32, NA, DOWN>(C, a0, a1, b, g, s, pdl);
+    case 64: return launch_gemm_t<64, NA, DOWN>(C, a0, a1, b, g, s, pdl);
+    case 128: return launch_gemm_t<128, NA, DOWN>(C, a0, a1, b, g, s, pdl);
     default:
-      if constexpr (NA <= 2) return launch_gemm_t<256, NA, DOWN>(C, a0, a1, b, g, s);
+      if constexpr (NA <= 2) return launch_gemm_t<256, NA, DOWN>(C, a0, a1, b, g, s, pdl);
       return fail(SP_ERR_VALUE, "token tile 256 with %d sub-tiles exceeds TMEM", NA);
   }
 }
@@ -739,7 +765,7 @@ static int launch_gemm(Context* C, int nt, const CUtensorMap& a0, const CUtensor
 // tile 2 * (p's row pair) + r and loads half of the x tile
 template <int NT, int NA>
 static int launch_gemm_pair_t(Context* C, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
-                              tc::GemmArgs g, cudaStream_t s) {
+                              tc::GemmArgs g, cudaStream_t s, bool pdl) {
   auto kern = tc::gemm_up_pair_kernel<NT, NA>;
   constexpr int STAGE = NA * tc::BM * tc::BK * 2 + (NT / 2) * tc::BK * 2;
   static bool attr_set = false;
@@ -750,17 +776,16 @@ static int launch_gemm_pair_t(Context* C, const CUtensorMap& a0, const CUtensorM
   const int pairs = (g.m_tiles + 1) / 2 * g.t_tiles;
   g.stages = std::max(2, std::min(6, (kSmemLimit - 1024 - 256) / STAGE));
   const size_t smem = size_t(g.stages) * STAGE + 1024 + 256;
-  kern<<<2 * pairs * g.ks, tc::kThreads, smem, s>>>(a0, a1, b, g);
-  SP_CUDA(cudaGetLastError());
+  SP_CUDA(launch_k(kern, dim3(2 * pairs * g.ks), dim3(tc::kThreads), smem, s, pdl, a0, a1, b, g));
   ++C->launches;
   return SP_OK;
 }
 
 template <int NA>
 static int launch_gemm_pair(Context* C, int nt, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
-                            const tc::GemmArgs& g, cudaStream_t s) {
+                            const tc::GemmArgs& g, cudaStream_t s, bool pdl) {
   switch (nt) {
-    case 256: return launch_gemm_pair_t<256, NA>(C, a0, a1, b, g, s);
+    case 256: return launch_gemm_pair_t<256, NA>(C, a0, a1, b, g, s, pdl);
     default: return fail(SP_ERR_VALUE, "CTA-pair up GEMM: no %d-token tile", nt);
   }
 }
@@ -773,7 +798,10 @@ static int split_k(int tiles, int k, int target) {
   return std::max(1, std::min(nkb, target / std::max(1, tiles)));
 }
 
-// up GEMM (fused SwiGLU / act) into a_tc, then down GEMM accumulated into the call's tc slice
+// up GEMM (fused SwiGLU / act) into a_tc, then down GEMM accumulated into the call's tc slice.
+// Every workspace is sized and every memset enqueued first, so the chain
+// gather -> up -> (swiglu_reduce) -> down is back-to-back kernels on `s` and
+// each one after the gather is launched with PDL (launch_k).
 static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype, int64_t ldx,
                         CallWs& w, const int32_t* dev_ids, int64_t T_e, int t0, int T, cudaStream_t s,
                         bool resident) {
@@ -782,21 +810,11 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
     w.tc_slice = w.S++;
     SP_CUDA(cudaMemsetAsync(w.part + size_t(w.tc_slice) * T_e * N, 0, size_t(T_e) * N * 4, s));
   }
-  // gathered bf16 x rows [T, M]
-  {
-    dim3 grid(unsigned(std::min<int64_t>((M + 255) / 256, 16)), unsigned(T));
-    tc::gather_rows_bf16_kernel<<<grid, 256, 0, s>>>(x, xdtype, ldx, dev_ids, t0, T, int(M), w.x_tc, L->ldm);
-    SP_CUDA(cudaGetLastError());
-    ++C->launches;
-  }
   const int nt = T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256;
   const int t_tiles = int((T + nt - 1) / nt);
   // HBM-resident blocks spread over every SM; streamed chunks hide under their copy
   const int target = resident ? C->num_sms : 32;
-  CUtensorMap tx, tw1, tw3, ta, tw2;
-  SP_TRY(make_tmap(&tw1, b.base, M, R, L->ldm * 2, tc::BK, tc::BM));
-  SP_TRY(make_tmap(&tw3, L->d.gated ? b.base + b.w3_off : b.base, M, R, L->ldm * 2, tc::BK, tc::BM));
-  SP_TRY(make_tmap(&tx, w.x_tc, M, T, L->ldm * 2, tc::BK, nt));
+  const int na = L->d.gated ? 2 : 1;
   tc::GemmArgs up{};
   up.mode = L->d.gated ? tc::kUpGated : tc::kUpPlain;
   up.act = L->d.act;
@@ -808,36 +826,12 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
   up.ks = split_k(up.m_tiles * t_tiles, int(M), target);
   up.a_out = w.a_tc;
   up.lda = w.ld_a;
-  const int na = L->d.gated ? 2 : 1;
   if (up.ks > 1) {
     // split partials of the pre-activations, finished by swiglu_reduce_kernel
     up.zld = round_up(R, 4);
     SP_TRY(C->tc_z.ensure(size_t(up.ks) * na * T * up.zld * 4, s));
     up.z = static_cast<float*>(C->tc_z.p);
   }
-  if (g_tc_pair && nt == 256) {
-    // x tile split across the two SMs of a CTA pair: 25 % fewer bytes into each SM.
-    // Measured (ncu, 14336-row expert): T = 512 up GEMM 153 -> 141 us, T = 256
-    // expert 134 -> 129 us; at 64/128-token tiles it was within +-4 % either way.
-    CUtensorMap txh;
-    SP_TRY(make_tmap(&txh, w.x_tc, M, T, L->ldm * 2, tc::BK, nt / 2));
-    if (L->d.gated)
-      SP_TRY((launch_gemm_pair<2>(C, nt, tw1, tw3, txh, up, s)));
-    else
-      SP_TRY((launch_gemm_pair<1>(C, nt, tw1, tw1, txh, up, s)));
-  } else if (L->d.gated) {
-    SP_TRY((launch_gemm<2, false>(C, nt, tw1, tw3, tx, up, s)));
-  } else {
-    SP_TRY((launch_gemm<1, false>(C, nt, tw1, tw1, tx, up, s)));
-  }
-  if (up.ks > 1) {
-    dim3 grid(unsigned((R / 4 + 127) / 128 + 1), unsigned(T));
-    tc::swiglu_reduce_kernel<<<grid, 128, 0, s>>>(up.z, up.ks, na, T, int(R), up.zld, L->d.act, w.a_tc, w.ld_a);
-    SP_CUDA(cudaGetLastError());
-    ++C->launches;
-  }
-  SP_TRY(make_tmap(&tw2, b.base + b.w2_off, N, R, L->ldn * 2, 64, tc::BK));
-  SP_TRY(make_tmap(&ta, w.a_tc, R, T, w.ld_a * 2, tc::BK, nt));
   tc::GemmArgs dn{};
   dn.mode = tc::kDown;
   dn.rows = int(N);
@@ -861,7 +855,46 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
     dn.ks = 1;  // streamed chunk: hidden under its copy, accumulate into the tc slice
     dn.y = w.part + size_t(w.tc_slice) * T_e * N + size_t(t0) * N;
   }
-  return launch_gemm<sub, true>(C, nt, tw2, tw2, ta, dn, s);
+  CUtensorMap tx, tw1, tw3, ta, tw2;
+  SP_TRY(make_tmap(&tw1, b.base, M, R, L->ldm * 2, tc::BK, tc::BM));
+  SP_TRY(make_tmap(&tw3, L->d.gated ? b.base + b.w3_off : b.base, M, R, L->ldm * 2, tc::BK, tc::BM));
+  SP_TRY(make_tmap(&tx, w.x_tc, M, T, L->ldm * 2, tc::BK, nt));
+  SP_TRY(make_tmap(&tw2, b.base + b.w2_off, N, R, L->ldn * 2, 64, tc::BK));
+  SP_TRY(make_tmap(&ta, w.a_tc, R, T, w.ld_a * 2, tc::BK, nt));
+
+  // gathered bf16 x rows [T, M]
+  {
+    const size_t xel = xdtype == SP_BF16 ? 2 : 4;
+    const bool vec = M % 8 == 0 && (size_t(ldx) * xel) % 16 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0;
+    const int per = vec ? 8 : 1;
+    dim3 grid(unsigned(std::min<int64_t>((M / per + 255) / 256, 16)), unsigned(T));
+    tc::gather_rows_bf16_kernel<<<grid, 256, 0, s>>>(x, xdtype, ldx, dev_ids, t0, T, int(M), w.x_tc, L->ldm,
+                                                     vec ? 1 : 0);
+    SP_CUDA(cudaGetLastError());
+    ++C->launches;
+  }
+  if (g_tc_pair && nt == 256) {
+    // x tile split across the two SMs of a CTA pair: 25 % fewer bytes into each SM.
+    // Measured (ncu, 14336-row expert): T = 512 up GEMM 153 -> 141 us, T = 256
+    // expert 134 -> 129 us; at 64/128-token tiles it was within +-4 % either way.
+    CUtensorMap txh;
+    SP_TRY(make_tmap(&txh, w.x_tc, M, T, L->ldm * 2, tc::BK, nt / 2));
+    if (L->d.gated)
+      SP_TRY((launch_gemm_pair<2>(C, nt, tw1, tw3, txh, up, s, true)));
+    else
+      SP_TRY((launch_gemm_pair<1>(C, nt, tw1, tw1, txh, up, s, true)));
+  } else if (L->d.gated) {
+    SP_TRY((launch_gemm<2, false>(C, nt, tw1, tw3, tx, up, s, true)));
+  } else {
+    SP_TRY((launch_gemm<1, false>(C, nt, tw1, tw1, tx, up, s, true)));
+  }
+  if (up.ks > 1) {
+    dim3 grid(unsigned((R / 4 + 127) / 128 + 1), unsigned(T));
+    SP_CUDA(launch_k(tc::swiglu_reduce_kernel, grid, dim3(128), 0, s, true, static_cast<const float*>(up.z), up.ks,
+                     na, T, int(R), up.zld, int(L->d.act), w.a_tc, w.ld_a));
+    ++C->launches;
+  }
+  return launch_gemm<sub, true>(C, nt, tw2, tw2, ta, dn, s, true);
 }
 
 static FfnArgs ffn_args(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,

@@ -21,11 +21,12 @@ mk = lambda *s: (torch.randn(*s, device="cuda", generator=g) / 64).to(torch.bflo
 lay = NativeLayer(mk(H, M), mk(H, M), 0, 0, "silu", mk(H, M), dtype="bf16")
 nbytes = lay.placed_bytes()["gg"]
 scratch = torch.zeros(64 << 20, device="cuda")
-for T in (16, 64, 128, 256, 512):
+import os
+for T in [int(t) for t in os.environ.get("SP_PREFILL_T", "16 64 128 256 512").split()]:
     x = torch.randn(T, M, device="cuda").to(torch.bfloat16)
     ts = []
     for r in range(6):
-        scratch.add_(1.0)
+        scratch.sum()  # L2 flush by reading: a write would leave dirty lines whose write-back competes
         torch.cuda.synchronize()
         nat.trace_enable(True)
         forward_calls([CallSpec(lay)], x)
