@@ -19,9 +19,24 @@
  *     reference raises before computing (slicing_kernel.py:64-70,111-118).
  *   - Weights are copied into library-owned placement at layer creation
  *     (GG -> HBM, CC and CG -> pinned host, chunk-interleaved); activations
- *     and outputs stay caller-owned.
+ *     and outputs stay caller-owned.  This deviates from SURVEY.md 8(b)
+ *     ("the caller owns all weight buffers") on purpose: the CG block must
+ *     sit in pinned, chunk-interleaved host memory and the GG block in HBM
+ *     with 128-byte rows, which a caller's numpy / torch views are not; the
+ *     caller may free its copies after sp_layer_create (host RAM is held
+ *     twice only while both exist).  Caller-side CC is still possible:
+ *     sp_set_cc_executor runs the CC block through the caller's own code.
  *   - One device per process/thread context (sp_init); forwards on one device
  *     are serialised by the library.
+ *
+ * Limits (each violation is reported as SP_ERR_VALUE before any work):
+ *   - out_dim N <= 8192 for bf16 weights, <= 4096 for f32 (the decode kernel
+ *     keeps 4 W2 column vectors per thread: kMaxVec, csrc/kernels.cuh);
+ *   - model_dim M <= 16384 (the decode kernel's x tile, TT * roundup(M, 256)
+ *     floats <= 16384, so 4 tokens per launch up to M = 4096, 1 up to 16384);
+ *   - at most 32 calls per sp_forward_batch and 32 active experts per
+ *     sp_moe_forward (kMaxCalls: the finalize kernel's by-value call table).
+ *   All five BASELINE configs (M <= 8192, N <= 8192, <= 16 experts) fit.
  */
 #ifndef SLICED_H_
 #define SLICED_H_
@@ -33,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 3
+#define SP_ABI_VERSION 4
 
 typedef enum sp_status {
   SP_OK = 0,
@@ -158,6 +173,22 @@ int sp_moe_route(const float* router, int64_t model_dim, int n_experts, int top_
 int sp_moe_forward(const sp_layer_t* layers, int n_experts, const float* router, int top_k,
                    const void* x, int xdtype, int64_t T, void* y, int ydtype, unsigned flags,
                    void* stream);
+
+/* ---- caller-supplied CC executor (north star: "the CC slice runs on host
+ * threads through the reference CPU code") ------------------------------- */
+/* Called on the library's CC coordinator thread, concurrently with the GPU
+ * work of the same forward, once per call whose CC block is non-empty:
+ *   x    [rows, ldx] f32: the call's CC token rows (gathered, in call order)
+ *   y_cc [rows, out_dim] f32: to be OVERWRITTEN with
+ *        sum over hidden units h in [0, b1) of act(x W1[:, h]) (* x W3[:, h]) W2[h, :]
+ * `layer` identifies the expert (the caller maps it to its weights).  Return
+ * 0 on success; non-zero fails the forward with SP_ERR_VALUE.  It must not
+ * call back into this library. */
+typedef int (*sp_cc_fn)(void* user, sp_layer_t layer, const float* x, int64_t ldx, int64_t rows, float* y_cc,
+                        int64_t out_dim);
+/* Install (fn != NULL) or remove (NULL) the executor for every later forward
+ * on this context; the native AVX-512 / AMX CC kernels run when none is set. */
+int sp_set_cc_executor(sp_cc_fn fn, void* user);
 
 /* Host-only CC block (no GPU): y_cc[T, N] (f32) = sum over cc columns.  Used by
  * the CPU test suite and the host-core micro-benchmarks of the profile refit. */

@@ -64,7 +64,12 @@ class TraceRecord(C.Structure):
     ]
 
 
+# sp_cc_fn (include/sliced.h): user, layer, x [rows, ldx] f32, ldx, rows, y_cc [rows, out_dim] f32, out_dim
+CC_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_float), C.c_int64, C.c_int64,
+                    C.POINTER(C.c_float), C.c_int64)
+
 SIGNATURES = {
+    "sp_set_cc_executor": (C.c_int, [CC_FN, C.c_void_p]),
     "sp_abi_version": (C.c_int, []),
     "sp_layer_image_sizes": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
                                        C.POINTER(C.c_int32)]),
@@ -197,3 +202,36 @@ def stats() -> dict:
     launches, h2d = C.c_uint64(), C.c_uint64()
     check(lib().sp_stats(C.byref(launches), C.byref(h2d)))
     return {"kernel_launches": launches.value, "h2d_bytes": h2d.value}
+
+
+_cc_keepalive = None  # the installed CFUNCTYPE object must outlive every forward that may call it
+
+
+def set_cc_executor(fn) -> None:
+    """Run every CC block through ``fn(layer_handle, x, y_cc) -> None`` (numpy
+    views: x [rows, M'] f32 with M' >= model_dim, y_cc [rows, out_dim] f32 to
+    overwrite) on the library's CC coordinator thread, concurrently with the
+    forward's GPU work; ``None`` restores the native CC kernels."""
+    global _cc_keepalive
+    import numpy as np
+
+    if fn is None:
+        check(lib().sp_set_cc_executor(C.cast(None, CC_FN), None))
+        _cc_keepalive = None
+        return
+
+    def trampoline(_user, layer, x, ldx, rows, y, out_dim):
+        try:
+            xa = np.ctypeslib.as_array(x, shape=(rows, ldx))
+            ya = np.ctypeslib.as_array(y, shape=(rows, out_dim))
+            fn(int(layer or 0), xa, ya)
+            return 0
+        except Exception:  # reported as SP_ERR_VALUE by the forward
+            import traceback
+
+            traceback.print_exc()
+            return 1
+
+    cb = CC_FN(trampoline)
+    check(lib().sp_set_cc_executor(cb, None))
+    _cc_keepalive = cb

@@ -198,6 +198,10 @@ struct Context {
   std::vector<float> hscratch;
   std::unique_ptr<ThreadPool> pool;
   int host_threads = 1;
+  // caller-supplied CC executor (sp_set_cc_executor): when set, every CC block
+  // runs through it instead of the native host kernels
+  sp_cc_fn cc_fn = nullptr;
+  void* cc_user = nullptr;
   // CC coordinator: runs a forward's CC block (on `pool`) while the calling
   // thread keeps enqueueing GPU work -- Stream-A and Stream-B of PAPER.md:161
   // on separate host threads.
@@ -1342,6 +1346,8 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     // ---- CC block: submitted to the coordinator now, runs while we enqueue ----
     cc_async = need_cc && !(flags & SP_NO_CC_THREADS);
     const bool x_on_host_now = host_io || x_host_ready;
+    const sp_cc_fn cc_fn = C->cc_fn;
+    void* const cc_user = C->cc_user;
     cc_work = [=]() -> int {
       if (!x_on_host_now) {
         const cudaError_t e = cudaEventSynchronize(C->ev_x);
@@ -1372,10 +1378,22 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         bytes += double(L->cc_bytes);
       }
       const int cc_threads = (flags & SP_NO_CC_THREADS) ? 1 : C->host_threads;
-      if (g_cc_batch)
+      if (cc_fn) {
+        // the caller's CC code (e.g. the reference's numpy forward) on this thread
+        int k = 0;
+        for (int c = 0; c < n_calls; ++c) {
+          const sp_layer* L = calls[c].layer;
+          const int64_t Tcc = calls[c].tokens - calls[c].n_g;
+          if (L->d.b1 <= 0 || Tcc <= 0) continue;
+          const CCProblem& pr = probs[size_t(k++)];
+          if (cc_fn(cc_user, const_cast<sp_layer*>(L), pr.x, pr.ldx, Tcc, pr.y, N) != 0)
+            return fail(SP_ERR_VALUE, "the CC executor failed on call %d", c);
+        }
+      } else if (g_cc_batch) {
         cc_forward_batch(probs.data(), int(probs.size()), *C->pool, cc_threads);
-      else
+      } else {
         for (const CCProblem& pr : probs) cc_forward(pr, *C->pool, cc_threads);
+      }
       host_span(C, 3, SP_TRACE_CC, t_cc0, now_s(), bytes);
       return SP_OK;
     };
@@ -2222,6 +2240,15 @@ int sp_cc_forward_host(sp_layer_t L, const void* x, int xdtype, int64_t T, float
 int sp_round_bf16(const float* src, uint16_t* dst, int64_t n) {
   if (n < 0 || (n > 0 && (!src || !dst))) return fail(SP_ERR_VALUE, "NULL argument");
   round_bf16_host(src, dst, n);
+  return SP_OK;
+}
+
+int sp_set_cc_executor(sp_cc_fn fn, void* user) {
+  Context* C = ctx_or_null();
+  if (!C) return fail(SP_ERR_STATE, "sp_init has not been called");
+  std::lock_guard<std::mutex> g(C->mu);  // never while a forward is in flight
+  C->cc_fn = fn;
+  C->cc_user = fn ? user : nullptr;
   return SP_OK;
 }
 

@@ -17,6 +17,13 @@ modules define ``ShapeMismatch`` and ``TokenCountOutOfRange``).  The only
 other dependency is numpy.  ``tests/test_refbind.py`` drives it through a
 stand-in with the reference's signature.
 
+``use_reference_cc(True)`` runs every CC block through the reference's own
+CPU expression (``_activate(x @ w1_cc) @ w2_cc`` in fp64 numpy,
+``slicing_kernel.py:33-38,119-123``) via the ABI's CC-executor hook
+(``sp_set_cc_executor``), concurrently with the GPU's GG / CG work -- the
+north star's "CC slice on host threads through the reference CPU code".  The
+default is the library's native AVX-512 / AMX CC kernels.
+
 Library location: ``$SLICED_LIB``, else ``_native/libsliced.so`` next to this
 file.  Device: ``$SLICED_DEVICE`` (default 0).
 """
@@ -24,6 +31,7 @@ file.  Device: ``$SLICED_DEVICE`` (default 0).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import threading
 import weakref
@@ -50,10 +58,18 @@ class _Call(C.Structure):  # sp_call (include/sliced.h)
                 ("n_g", C.c_int64)]
 
 
+# sp_cc_fn (include/sliced.h)
+_CC_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_float), C.c_int64, C.c_int64,
+                     C.POINTER(C.c_float), C.c_int64)
+
 _lib = None
 _lock = threading.RLock()  # a GC finalizer may run while it is held
 # id(SlicedWeights) -> (weakref to it, {activation code: sp_layer_t, ...}, out_dim)
 _placed: dict[int, tuple] = {}
+# sp_layer_t -> (w1 cc block [M, b1], w2 cc block [b1, N], activation name): the
+# reference CC executor's operands (views of the caller's arrays)
+_cc_blocks: dict[int, tuple] = {}
+_cc_callback = None
 
 
 def _library():
@@ -76,6 +92,8 @@ def _library():
                                         C.POINTER(C.c_void_p)]
         lib.sp_layer_destroy.restype = C.c_int
         lib.sp_layer_destroy.argtypes = [C.c_void_p]
+        lib.sp_set_cc_executor.restype = C.c_int
+        lib.sp_set_cc_executor.argtypes = [_CC_FN, C.c_void_p]
         lib.sp_forward_batch.restype = C.c_int
         lib.sp_forward_batch.argtypes = [C.POINTER(_Call), C.c_int, C.c_void_p, C.c_int, C.c_int64,
                                          C.c_void_p, C.c_int, C.c_uint, C.c_void_p]
@@ -99,8 +117,46 @@ def _act_code(activation) -> int:
 
 def _destroy(handles: list) -> None:
     for h in handles:
+        _cc_blocks.pop(h, None)
         if _lib is not None and h:
             _lib.sp_layer_destroy(h)
+
+
+def _activate(name: str, z: np.ndarray) -> np.ndarray:
+    """The reference's activation (slicing_kernel.py:33-38), fp64."""
+    if name == "identity":
+        return z
+    if name == "silu":
+        return z / (1.0 + np.exp(-z))
+    from scipy.special import erf  # the reference's own erf
+
+    return 0.5 * z * (1.0 + erf(z / math.sqrt(2.0)))
+
+
+def _reference_cc(_user, layer, x_ptr, ldx, rows, y_ptr, out_dim) -> int:
+    try:
+        w1_cc, w2_cc, act = _cc_blocks[int(layer)]
+        x = np.ctypeslib.as_array(x_ptr, shape=(rows, ldx))[:, : w1_cc.shape[0]].astype(np.float64)
+        y = np.ctypeslib.as_array(y_ptr, shape=(rows, out_dim))
+        y[:] = _activate(act, x @ w1_cc) @ w2_cc  # slicing_kernel.py:122-123, the CC block
+        return 0
+    except Exception:
+        return 1
+
+
+def use_reference_cc(on: bool = True) -> None:
+    """Run CC blocks through the reference's fp64 numpy expression (True) or
+    the library's native CC kernels (False)."""
+    global _cc_callback
+    lib = _library()
+    with _lock:
+        if on:
+            cb = _CC_FN(_reference_cc)
+            _check(lib.sp_set_cc_executor(cb, None))
+            _cc_callback = cb  # kept alive while installed
+        else:
+            _check(lib.sp_set_cc_executor(C.cast(None, _CC_FN), None))
+            _cc_callback = None
 
 
 def place(sliced, activation):
@@ -130,6 +186,9 @@ def place(sliced, activation):
             entry = (ref, handles, int(w2.shape[1]))
             _placed[key] = entry
         entry[1][code] = handle.value
+        act_name = next(k for k, v in _ACT.items() if v == code)
+        _cc_blocks[handle.value] = (np.asarray(sliced.w1_blocks[0], dtype=np.float64),
+                                    np.asarray(sliced.w2_blocks[0], dtype=np.float64), act_name)
     return handle.value, entry[2]
 
 

@@ -51,7 +51,58 @@ def test_decoder_matches_oracle_moe():
         xa = m.decode_step(xa, pos)
         xb = ref.decode_step(xb, pos)
     err = orc.max_rel_error(xa.float().cpu().numpy(), xb.float().cpu().numpy())
+    # whole decoder (attention + bf16 residual stream over 3 layers x 4 steps); each
+    # MoE call alone is held to 1e-2 in test_every_moe_call_in_the_decoder_matches_the_oracle
     assert err <= 3e-2, err
+    m.release()
+
+
+def test_every_moe_call_in_the_decoder_matches_the_oracle():
+    """Inside the decode loop, every sliced MoE call (the path under test) is
+    held to the north-star bf16 bound (<= 1e-2) against the fp64 oracle on
+    the same input h.  The whole-decoder comparison above allows 3e-2: it also
+    carries the torch attention / RMSNorm and the bf16 residual stream across
+    layers, which are outside the sliced path."""
+    import torch
+
+    from paper_2411_15715_b200 import _native as nat
+    from paper_2411_15715_b200.model import DecoderConfig, SlicedMixtral
+    from paper_2411_15715_b200.schedule import SlicingRates
+    from paper_2411_15715_b200.sliced import SlicedFFN
+
+    nat.init(0)
+    cfg = DecoderConfig(layers=3, distinct=2, model_dim=256, hidden_dim=640, experts=4, top_k=2, heads=4,
+                        kv_heads=2, max_seq=32)
+    rng = np.random.default_rng(5)
+    weights = {}
+
+    def factory(d):
+        ws = [tuple(rng.standard_normal(s).astype(np.float32) / 8 for s in ((640, 256), (640, 256), (256, 640)))
+              for _ in range(cfg.experts)]
+        weights[d] = [tuple(orc.bf16_round(a) for a in w) for w in ws]
+        return [SlicedFFN(w1t, w2t, SlicingRates(0.25, 0.25, 0.5), w3t=w3t, chunk_rows=128) for w1t, w3t, w2t in ws]
+
+    m = SlicedMixtral(cfg, SlicingRates(0.25, 0.25, 0.5), experts_factory=factory)
+    seen = []
+    inner = m._moe
+
+    def checked(d, h, out=None):
+        y = inner(d, h, out=out)
+        torch.cuda.synchronize()
+        hq = h.float().cpu().numpy().astype(np.float64)
+        experts = [(w1t.T, w3t.T, w2t.T) for w1t, w3t, w2t in weights[d]]
+        router = m.routers[d].astype(np.float32).astype(np.float64)
+        ref = orc.moe_forward(hq, experts, router, cfg.top_k)
+        seen.append(orc.max_rel_error(y.float().cpu().numpy(), ref))
+        return y
+
+    m._moe = checked
+    x = (torch.randn(1, 256, device="cuda", generator=torch.Generator(device="cuda").manual_seed(4)) * 0.5).to(
+        torch.bfloat16)
+    for pos in range(4):
+        x = m.decode_step(x, pos)
+    assert len(seen) == 4 * cfg.layers
+    assert max(seen) <= 1e-2, seen
     m.release()
 
 

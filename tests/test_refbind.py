@@ -70,8 +70,9 @@ def test_binding_imports_only_numpy_ctypes_and_errors():
         if isinstance(node, ast.Import):
             mods |= {a.name.split(".")[0] for a in node.names}
         elif isinstance(node, ast.ImportFrom):
-            mods.add(("." * node.level) + (node.module or ""))
-    assert mods <= {"__future__", "ctypes", "os", "threading", "weakref", "pathlib", "numpy", ".errors"}, mods
+            mods.add(("." * node.level) + (node.module or "") if node.level else node.module.split(".")[0])
+    assert mods <= {"__future__", "ctypes", "math", "os", "threading", "weakref", "pathlib", "numpy", "scipy",
+                    ".errors"}, mods
 
 
 def test_argument_errors_before_any_device_work():
@@ -136,3 +137,45 @@ def test_refbind_places_once_and_frees_on_gc():
     # empty token batch: same shape contract as the reference
     s2 = standin_slice_weights(w1, w2, StandInRates(0.0, 0.0, 1.0))
     assert refbind.mlp_forward_sliced(np.zeros((0, M)), s2, Activation.SILU).shape == (0, N)
+
+
+@pytest.mark.gpu
+def test_reference_cc_executor_runs_the_cc_block_through_numpy():
+    """use_reference_cc: the CC block is the reference's own fp64 numpy
+    expression, run by the library's coordinator thread next to the GPU work;
+    the result still matches the reference goldens, and the native CC kernels
+    are back once it is switched off."""
+    from paper_2411_15715_b200 import _native as nat
+
+    npz = np.load(GOLDEN / "forward_golden.npz")
+    meta = json.loads(bytes(npz["meta_json"]).decode())
+    calls = []
+    orig = refbind._reference_cc
+
+    def counting(*a):
+        calls.append(a[4])  # rows
+        return orig(*a)
+
+    refbind._reference_cc = counting
+    try:
+        refbind.use_reference_cc(True)
+        n_cc = 0
+        for case in meta["cases"]:
+            k = case["key"]
+            x, w1, w2 = npz[f"{k}_x"], npz[f"{k}_w1"], npz[f"{k}_w2"]
+            s = standin_slice_weights(w1, w2, StandInRates(*(float.fromhex(v) for v in case["rates"])))
+            got = refbind.mlp_forward_sliced(x, s, case["act"], case["n_g"])
+            assert orc.max_rel_error(got, npz[f"{k}_sliced"]) <= FP32_TOL, k
+            if s.block_widths[0] > 0 and x.shape[0] - case["n_g"] > 0:
+                n_cc += 1
+            refbind.release(s)
+        assert len(calls) == n_cc > 0
+    finally:
+        refbind.use_reference_cc(False)
+        refbind._reference_cc = orig
+    before = len(calls)
+    rng = np.random.default_rng(3)
+    s = standin_slice_weights(rng.uniform(-1, 1, (32, 200)), rng.uniform(-1, 1, (200, 16)), StandInRates(0.5, 0.2, 0.3))
+    refbind.mlp_forward_sliced(rng.uniform(-1, 1, (2, 32)), s, "silu")
+    assert len(calls) == before  # native CC again
+    assert nat.lib().sp_abi_version() >= 4
