@@ -9,6 +9,6 @@ for r in $(seq $ROUNDS); do
 import json,sys; d=json.loads(sys.stdin.read()); rf=d.get('roofline') or {}
 print('$VAR=$v', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), 'ms', round(d['ms_per_step'],4),
       'gg_frac', rf.get('frac') and round(rf['frac'],3), 'dev', rf.get('frac_device_span') and round(rf['frac_device_span'],3),
-      'rates', d['config'].get('rates'))"
+      'rates', (d.get('split') or {}).get('rates'))"
   done
 done 2>&1 | tee gpurun_out/ab_$VAR.log
