@@ -69,7 +69,10 @@ def parse(argv=None):
                          "extension planner.solve_ng_layer (experts share the link and the host)")
     ap.add_argument("--ng-frac", type=float, default=-1.0,
                     help="cfg3 study only: n_g = round(frac * T_e) instead of solve_ng (landscape sweeps)")
-    ap.add_argument("--prompt-profile", default=str(ROOT / "profiles" / "b200_prompt.json"))
+    ap.add_argument("--prompt-profile", default="",
+                    help="prompt-phase profile (default: profiles/b200_prompt.json, host CC sampled at 32 tokens, "
+                         "for solve_ng; profiles/b200_prompt_t128.json, sampled at an expert's 128-token share, "
+                         "for --token-plan layer)")
     ap.add_argument("--batch", type=int, default=1, help="decode tokens per step per GPU")
     ap.add_argument("--budget-frac", type=float, default=0.5,
                     help="GPU budget as a fraction of each expert's bytes (planner units)")
@@ -812,6 +815,9 @@ def run_prefill_decode(args):
     torch.cuda.set_device(device)
     nat.init(local)
     rates, budget, source, _ = plan_rates(args, 1)
+    if not args.prompt_profile:
+        args.prompt_profile = str(ROOT / "profiles" / ("b200_prompt_t128.json" if args.token_plan == "layer"
+                                                       else "b200_prompt.json"))
     p_profile, p_source = load_profile(args.prompt_profile)
     if p_source.startswith("fallback"):
         p_profile, p_source = load_profile(args.profile)
@@ -973,7 +979,7 @@ def run_model(args):
     # solve_ng's token split on the prompt-phase profile), timed
     import paper_2411_15715_b200 as sp
 
-    p_profile, _ = load_profile(args.prompt_profile)
+    p_profile, _ = load_profile(args.prompt_profile or str(ROOT / "profiles" / "b200_prompt.json"))
     layer_spec = sp.LayerSpec(args.model_dim, args.hidden_dim, n_gemms=3, precision=sp.Precision.FP16)
     ng_cache = {}
 

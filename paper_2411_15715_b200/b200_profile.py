@@ -273,7 +273,7 @@ def launch_samples(torch, reps=20):
 
 
 def measure(phase: str = "decode", quick: bool = False, load: str = "concurrent",
-            tokens: int = 1, prompt_insitu: bool = False) -> list[ProfileSample]:
+            tokens: int = 1, prompt_insitu: bool = False, cpu_tokens: int = 32) -> list[ProfileSample]:
     """decode: ``tokens`` per expert everywhere (1 = single-token decode; 2..8
     for batched decode, where each active expert sees a few tokens).  prompt:
     the GPU GEMM at T = 128 tokens (an expert's share of a 512-token top-2
@@ -284,7 +284,7 @@ def measure(phase: str = "decode", quick: bool = False, load: str = "concurrent"
     import torch
 
     nat.init(0)
-    gpu_tokens, cpu_tokens = (tokens, tokens) if phase == "decode" else (128, 32)
+    gpu_tokens, cpu_tokens = (tokens, tokens) if phase == "decode" else (128, cpu_tokens)
     widths = [256, 1024, 2048, 4096, 7168, 10240, 14336]
     cpu_widths = [128, 256, 512, 1024, 2048, 4096] if phase == "decode" else [256, 1024, 2048, 4096]
     if quick:
@@ -330,14 +330,18 @@ def main(argv=None) -> None:
                     help="prompt phase: sample the CC block inside real prompt steps (see measure())")
     ap.add_argument("--tokens", type=int, default=1,
                     help="decode: tokens per expert (batched decode); writes b200_decode_t<T>.json for T > 1")
+    ap.add_argument("--cpu-tokens", type=int, default=32,
+                    help="prompt phase: tokens per host CC sample (32: the per-expert solve_ng profile; "
+                         "128, an expert's share of a 512-token prompt: the layer planner's)")
+    ap.add_argument("--tag", default="", help="file tag suffix (b200_<phase><tag>.json)")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--load", default="concurrent", choices=["concurrent", "isolated"],
                     help="sample the host-side rates under each other's host-DRAM load (default) or alone")
     args = ap.parse_args(argv)
     out = Path(args.out)
     out.mkdir(parents=True, exist_ok=True)
-    samples = measure(args.phase, args.quick, args.load, args.tokens, args.prompt_insitu)
-    tag = args.phase if args.phase == "prompt" or args.tokens == 1 else f"{args.phase}_t{args.tokens}"
+    samples = measure(args.phase, args.quick, args.load, args.tokens, args.prompt_insitu, args.cpu_tokens)
+    tag = (args.phase if args.phase == "prompt" or args.tokens == 1 else f"{args.phase}_t{args.tokens}") + args.tag
     write_samples_csv(samples, out / f"b200_samples_{tag}.csv")
     prof, warns = fit_profile(samples, f"b200-{tag}" + ("" if args.load == "concurrent" else "-isolated"))
     (out / f"b200_{tag}.json").write_bytes(save_profile(prof))
