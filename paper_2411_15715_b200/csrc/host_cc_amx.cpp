@@ -11,9 +11,9 @@
 //   up    per 16-row hidden slab (dynamic cursor), per 2 token groups:
 //           C[h][t] += W1t[h][k:k+32] . xp[g][k/2..][t]   A = weight rows as stored
 //         a[t][h] = bf16(act(C1) [* C3])  (AVX-512, into one shared [T16][b1p] array)
-//   down  per thread a contiguous range of output columns, repacked W2 rows in
-//         VNNI pairs per 128-column round; 4 accumulator tiles (2 token groups
-//         x 2 column tiles) run over the WHOLE hidden range before one store:
+//   down  rounds of 128 output columns (dynamic cursor), W2 rows repacked in
+//         VNNI pairs per round; 4 accumulator tiles (2 token groups x 2 column
+//         tiles) run over the WHOLE hidden range before one store:
 //           Y[t][n] = sum_h a[t][h] W2[h][n]
 // The down phase splits columns, not hidden rows, so there are no partial
 // slices to reduce and each output element is summed in one fixed hidden order
@@ -310,22 +310,22 @@ AMX_TARGET void up_worker(const AmxShared& S) {
     fprintf(stderr, "  up thread: %d slabs, kcycles tiles %llu act %llu\n", slabs, c_up >> 10, c_act >> 10);
 }
 
-// ---- phase 2: the down GEMM over a contiguous range of output columns ----
-AMX_TARGET void down_worker(const AmxShared& S, int tid, int nthr) {
+// ---- phase 2: the down GEMM, kRoundCols output columns at a time ----
+AMX_TARGET void down_worker(const AmxShared& S, std::atomic<int64_t>* rounds, int tid) {
   const CCProblem& p = S.p;
   const int64_t T = p.T, N = p.N, T16 = S.T16, G16 = S.G16, n16 = S.n16, b1p = S.b1p, ldn = S.ldn;
-  const int64_t ntiles = n16 / 16;
-  const int64_t j0 = ntiles * tid / nthr, j1 = ntiles * (tid + 1) / nthr;  // column tiles of this thread
-  if (j1 <= j0) return;
+  const int64_t ntiles = n16 / 16, per = kRoundCols / 16;
   static thread_local Scratch w2ps, ys;
   uint16_t* const w2p = w2ps.get(size_t(b1p / 2 * kRoundCols * 2));
   float* const ybuf = reinterpret_cast<float*>(ys.get(size_t(T16 * kRoundCols * 2)));  // [T16][nr] fp32
   tile_config();
   static const bool prof = getenv("SP_AMX_PROF") != nullptr;
   unsigned long long c_rep = 0, c_dn = 0, tc = 0;
-  for (int64_t jr = j0; jr < j1; jr += kRoundCols / 16) {
+  for (;;) {  // rounds of kRoundCols output columns, claimed dynamically (the host's vCPUs differ in speed)
+    const int64_t jr = per * rounds->fetch_add(1, std::memory_order_relaxed);
+    if (jr >= ntiles) break;
     if (prof) tc = __rdtsc();
-    const int64_t je = std::min(j1, jr + kRoundCols / 16);
+    const int64_t je = std::min(ntiles, jr + per);
     const int64_t n0 = 16 * jr, nr = 16 * (je - jr);
     // W2 rows of the round's columns in VNNI pairs: w2p[kp][n][e] = W2[2 kp + e][n0 + n], 0 past b1
     for (int64_t kp = 0; kp < b1p / 2; ++kp) {
@@ -477,7 +477,9 @@ void cc_forward_amx(const CCProblem& p, ThreadPool& pool, int threads) {
   AmxShared S{p, T16, G16, K32, KP, n16, b1p, p.ldm * 2, p.ldn, (p.b1 + 15) / 16, xp, a, chunk_of.data(), &cursor};
   pool.run(int(std::min<int64_t>(nthr, S.n_slabs)), [&](int, int) { up_worker(S); });
   const auto t2 = std::chrono::steady_clock::now();
-  pool.run(int(std::min<int64_t>(nthr, n16 / 16)), [&](int tid, int n) { down_worker(S, tid, n); });
+  std::atomic<int64_t> rounds{0};
+  pool.run(int(std::min<int64_t>(nthr, (n16 / 16 + kRoundCols / 16 - 1) / (kRoundCols / 16))),
+           [&](int tid, int) { down_worker(S, &rounds, tid); });
   if (prof) {
     const auto t3 = std::chrono::steady_clock::now();
     auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
