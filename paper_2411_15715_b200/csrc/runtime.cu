@@ -1176,7 +1176,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   // ---- validate everything before enqueuing anything ----
   if (n_calls < 1 || n_calls > kMaxCalls)
     return fail(SP_ERR_VALUE, "n_calls must lie in [1, %d], got %d", kMaxCalls, n_calls);
-  if (T < 1) return fail(SP_ERR_SHAPE, "input must have at least one row, got T=%lld", (long long)T);
+  if (T < 0) return fail(SP_ERR_SHAPE, "negative row count T=%lld", (long long)T);
   if ((xdtype != SP_F32 && xdtype != SP_BF16) || (ydtype != SP_F32 && ydtype != SP_BF16))
     return fail(SP_ERR_VALUE, "x/y dtype must be SP_F32 or SP_BF16");
   // SP_X_TO_BF16: the caller's f32 x is rounded into the bf16 staging copy; every
@@ -1216,6 +1216,9 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   }
   if (max_token_tile(M) == 0)
     return fail(SP_ERR_VALUE, "model_dim %lld exceeds the %d-float x tile", (long long)M, kMaxTileFloats);
+  // no rows: nothing to compute (the reference returns an empty [0, N] output,
+  // slicing_kernel.py:119); every call was checked to cover zero rows above
+  if (T == 0) return SP_OK;
   const bool host_io = flags & SP_IO_HOST;
   const double t_call = now_s();
 
@@ -1796,8 +1799,10 @@ static int moe_route(const float* router, int64_t M, int E, int k, const void* x
 
 static int moe_forward(Context* C, const sp_layer_t* layers, int E, const float* router, int k, const void* x,
                        int xdtype, int64_t T, void* y, int ydtype, unsigned flags, cudaStream_t user) {
-  if (!layers || !router || !x || !y) return fail(SP_ERR_VALUE, "NULL argument");
-  if (T < 1) return fail(SP_ERR_SHAPE, "input must have at least one row, got T=%lld", (long long)T);
+  if (!layers || !router) return fail(SP_ERR_VALUE, "NULL argument");
+  if (T < 0) return fail(SP_ERR_SHAPE, "negative row count T=%lld", (long long)T);
+  if (T == 0) return SP_OK;  // no tokens: nothing to route or compute
+  if (!x || !y) return fail(SP_ERR_VALUE, "NULL argument");
   const sp_layer* any = nullptr;
   for (int e = 0; e < E; ++e)
     if (layers[e]) any = layers[e];
@@ -1972,6 +1977,14 @@ static int validate_desc(const sp_layer_desc& d) {
                 (long long)d.b1, (long long)d.b2, (long long)d.hidden_dim);
   if (d.act < 0 || d.act > 2) return fail(SP_ERR_VALUE, "unknown activation %d", d.act);
   if (d.wdtype != SP_F32 && d.wdtype != SP_BF16) return fail(SP_ERR_VALUE, "unknown weight dtype");
+  // the decode kernel's limits (include/sliced.h "Limits"), refused at creation
+  // rather than at the first forward
+  const int64_t max_n = int64_t(kMaxVec) * kConsumers * 32 * (d.wdtype == SP_BF16 ? 8 : 4);
+  if (d.out_dim > max_n)
+    return fail(SP_ERR_VALUE, "out_dim %lld exceeds %lld for %s weights", (long long)d.out_dim, (long long)max_n,
+                d.wdtype == SP_BF16 ? "bf16" : "f32");
+  if (max_token_tile(d.model_dim) == 0)
+    return fail(SP_ERR_VALUE, "model_dim %lld exceeds the %d-float x tile", (long long)d.model_dim, kMaxTileFloats);
   return SP_OK;
 }
 
