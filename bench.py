@@ -137,6 +137,14 @@ def rank_host_threads() -> int:
     return int(os.environ.get("SP_HOST_THREADS", "0") or 0) or (os.cpu_count() or PROFILE_HOST_THREADS)
 
 
+def prompt_profile_path(args):
+    """--prompt-profile, else the fitted prompt profile the token plan uses
+    (128-token fit for the per-layer plan, 32-token fit for solve_ng)."""
+    if args.prompt_profile:
+        return args.prompt_profile
+    return str(ROOT / "profiles" / ("b200_prompt_t128.json" if args.token_plan == "layer" else "b200_prompt.json"))
+
+
 def load_profile(path):
     """The fitted profile; with fewer host threads per rank than it was measured
     with (one process per GPU sharing the host), the CPU terms are scaled by
@@ -144,8 +152,8 @@ def load_profile(path):
     from paper_2411_15715_b200 import costs
     from paper_2411_15715_b200.b200_profile import FALLBACK_DECODE
 
-    p = Path(path)
-    if p.exists():
+    p = Path(path) if path else None
+    if p is not None and p.is_file():
         prof, src = costs.load_profile(p), str(p.relative_to(ROOT) if p.is_relative_to(ROOT) else p)
     else:
         prof, src = costs.profile_from_dict(FALLBACK_DECODE), "fallback (b200_profile.FALLBACK_DECODE)"
@@ -815,9 +823,7 @@ def run_prefill_decode(args):
     torch.cuda.set_device(device)
     nat.init(local)
     rates, budget, source, _ = plan_rates(args, 1)
-    if not args.prompt_profile:
-        args.prompt_profile = str(ROOT / "profiles" / ("b200_prompt_t128.json" if args.token_plan == "layer"
-                                                       else "b200_prompt.json"))
+    args.prompt_profile = prompt_profile_path(args)
     p_profile, p_source = load_profile(args.prompt_profile)
     if p_source.startswith("fallback"):
         p_profile, p_source = load_profile(args.profile)

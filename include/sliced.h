@@ -155,7 +155,7 @@ int sp_layer_reslice(sp_layer_t layer, int64_t b1, int64_t b2, sp_layer_t* out);
  * x: [T, M] (xdtype), y: [T, N] (ydtype), overwritten.  Rows no call touches
  * are zero.  T = 0 (and every call covering 0 rows) is a valid empty forward
  * that returns SP_OK without touching the device, as the reference returns an
- * empty output.  With SP_IO_DEVICE the call returns once the CC slice is done and
+ * empty output (x and y may then be NULL).  With SP_IO_DEVICE the call returns once the CC slice is done and
  * the GPU work is enqueued (ordered after prior work on `stream`, and `stream`
  * is ordered after it); with SP_IO_HOST it returns with y written. */
 int sp_forward_batch(const sp_call* calls, int n_calls, const void* x, int xdtype, int64_t T,

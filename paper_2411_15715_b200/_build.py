@@ -16,7 +16,9 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_native"
 LIB = OUT_DIR / "libsliced.so"
 SOURCES = ["runtime.cu", "host_cc.cpp", "host_cc_amx.cpp"]
-HEADERS = ["kernels.cuh", "gemm_tc.cuh", "host_cc.h", "../../include/sliced.h"]
+# every header under csrc/ (a new one is picked up without editing this list) + the ABI header
+HEADERS = sorted(p.name for p in CSRC.glob("*.cuh")) + sorted(p.name for p in CSRC.glob("*.h")) + [
+    "../../include/sliced.h"]
 
 NVCC_FLAGS = [
     "-O3",

@@ -175,7 +175,7 @@ def test_cfg3_prompt_layer_with_solve_ng_split(torch, monkeypatch):
     from paper_2411_15715_b200.sliced import SlicedMoE, moe_route
 
     args, rates = bench_plan(monkeypatch, "--config", "cfg3")
-    p_profile, _ = bench.load_profile(args.prompt_profile)
+    p_profile, _ = bench.load_profile(bench.prompt_profile_path(args))
     spec = sp.LayerSpec(args.model_dim, args.hidden_dim, n_gemms=3, precision=sp.Precision.FP16)
     weights = make_weights(torch, args.experts, args.model_dim, args.hidden_dim, "bf16")
     experts = place(weights, rates, "bf16")
