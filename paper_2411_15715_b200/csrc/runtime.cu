@@ -35,7 +35,6 @@
 #include "host_cc.h"
 #include "kernels.cuh"
 #include "gemm_tc.cuh"
-#include "expert_tc.cuh"
 #include <cudaTypedefs.h>
 
 
@@ -196,9 +195,6 @@ struct Context {
   DevBuf tc_partial;  // split-K partial tiles of the tensor-core GEMMs
   DevBuf tc_tickets;  // per-tile split tickets (zero, re-armed by the last split)
   DevBuf tc_z;        // up-GEMM split partials of the pre-activations
-  DevBuf tc_fws;      // expert_tc_kernel: split-tile partials (up pre-activations, down outputs)
-  DevBuf tc_fflags;   // expert_tc_kernel: per-tile epoch flags (zeroed on allocation)
-  uint32_t tc_epoch = 0;
   std::vector<float> hscratch;
   std::unique_ptr<ThreadPool> pool;
   int host_threads = 1;
@@ -607,10 +603,6 @@ static int preload_kernels() {
   SP_TRY(preload(tc::swiglu_reduce_kernel, false));
   SP_TRY(preload(tc::gemm_up_pair_kernel<256, 1>, true));
   SP_TRY(preload(tc::gemm_up_pair_kernel<256, 2>, true));
-  SP_TRY(preload(tc::expert_tc_kernel<16>, true));
-  SP_TRY(preload(tc::expert_tc_kernel<32>, true));
-  SP_TRY(preload(tc::expert_tc_kernel<64>, true));
-  SP_TRY(preload(tc::expert_tc_kernel<128>, true));
   return preload(tc::gather_rows_bf16_kernel, false);
 }
 
@@ -811,108 +803,6 @@ static int split_k(int tiles, int k, int target) {
 }
 
 static const int64_t g_test_fail_after_cc = env_int("SP_TEST_FAIL_AFTER_CC", 0);
-// SP_TC_FUSED=1: resident blocks at <= 128 tokens run expert_tc_kernel (experiment,
-// slower than the chain: profiles/r2/expert_tc_experiment.txt)
-// below instead of expert_tc_kernel
-static const bool g_tc_fused = env_int("SP_TC_FUSED", 0) != 0;
-
-constexpr int kFusedMinUnits = 8;
-static bool use_fused(const sp_layer* L, int T, bool resident) {
-  return g_tc_fused && resident && T >= 1 && T <= tc::kFusedMaxNT && L->d.out_dim % 4 == 0;
-}
-
-// Slots a tile of `nk` units needs: the most CTAs any tile's units fall on.
-static int max_contributors(int tiles, int nk, int G) {
-  const int units = tiles * nk;
-  int q = 1;
-  for (int t = 0; t < tiles; ++t)
-    q = std::max(q, tc::cta_of(t * nk + nk - 1, units, G) - tc::cta_of(t * nk, units, G) + 1);
-  return q;
-}
-
-// A resident block at <= 128 tokens: gather, then ONE persistent launch
-// (expert_tc_kernel) computing up + act/gate + down into one new output slice.
-static int run_block_fused(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype,
-                           int64_t ldx, CallWs& w, const int32_t* dev_ids, int64_t T_e, int t0, int T,
-                           cudaStream_t s) {
-  const int64_t M = L->d.model_dim, N = L->d.out_dim, R = b.rows;
-  const int nt = T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : 128;
-  tc::FusedArgs g{};
-  g.R = int(R);
-  g.M = int(M);
-  g.N = int(N);
-  g.T = T;
-  g.act = L->d.act;
-  g.gated = L->d.gated ? 1 : 0;
-  g.nkU = int((M + tc::BK - 1) / tc::BK);
-  g.mU = int((R + tc::BM - 1) / tc::BM);
-  g.U = g.nkU * g.mU;
-  g.nkD = int((R + tc::BK - 1) / tc::BK);
-  g.mD = int((N + tc::kDownCols - 1) / tc::kDownCols);
-  g.D = g.nkD * g.mD;
-  // at least ~8 units (256 KB of weights) per CTA and phase: a small block (a
-  // streamed chunk) on every SM would split each tile over dozens of CTAs
-  g.G = int(std::max<int64_t>(1, std::min<int64_t>(C->num_sms, (int64_t(g.U) + g.D) / (2 * kFusedMinUnits))));
-  g.GU = std::min(g.G, g.U);
-  g.GD = std::min(g.G, g.D);
-  g.QU = max_contributors(g.mU, g.nkU, g.GU);
-  g.QD = max_contributors(g.mD, g.nkD, g.GD);
-  const size_t up_floats = size_t(g.mU) * g.QU * 2 * nt * tc::BM;
-  const size_t dn_floats = size_t(g.mD) * g.QD * nt * tc::kDownCols;
-  SP_TRY(C->tc_fws.ensure((up_floats + dn_floats) * 4, s));
-  const size_t nflags = size_t(g.mU) * (g.QU + 1) + size_t(g.mD) * g.QD;
-  if (nflags * 4 > C->tc_fflags.n) {
-    SP_TRY(C->tc_fflags.ensure(nflags * 4, s));
-    SP_CUDA(cudaMemsetAsync(C->tc_fflags.p, 0, C->tc_fflags.n, s));
-  }
-  if (++C->tc_epoch == 0) {  // wrapped: stale flags could read as this launch's
-    SP_CUDA(cudaMemsetAsync(C->tc_fflags.p, 0, C->tc_fflags.n, s));
-    C->tc_epoch = 1;
-  }
-  g.epoch = C->tc_epoch;
-  g.ws_up = static_cast<float*>(C->tc_fws.p);
-  g.ws_dn = g.ws_up + up_floats;
-  g.up_flag = static_cast<uint32_t*>(C->tc_fflags.p);
-  g.ready = g.up_flag + size_t(g.mU) * g.QU;
-  g.dn_flag = g.ready + g.mU;
-  g.a_out = w.a_tc;
-  g.lda = w.ld_a;
-  g.stamps = C->stamps;
-  // one new output slice; its rows outside [t0, t0 + T) must read as zero
-  if (t0 > 0 || T < T_e) SP_CUDA(cudaMemsetAsync(w.part + size_t(w.S) * T_e * N, 0, size_t(T_e) * N * 4, s));
-  g.y = w.part + size_t(w.S) * T_e * N + size_t(t0) * N;
-  g.ldy = N;
-  w.S += 1;
-
-  CUtensorMap tx, tw1, tw3, ta, tw2;
-  SP_TRY(make_tmap(&tw1, b.base, M, R, L->ldm * 2, tc::BK, tc::BM));
-  SP_TRY(make_tmap(&tw3, L->d.gated ? b.base + b.w3_off : b.base, M, R, L->ldm * 2, tc::BK, tc::BM));
-  SP_TRY(make_tmap(&tx, w.x_tc, M, T, L->ldm * 2, tc::BK, nt));
-  SP_TRY(make_tmap(&tw2, b.base + b.w2_off, N, R, L->ldn * 2, 64, tc::BK));
-  SP_TRY(make_tmap(&ta, w.a_tc, R, T, w.ld_a * 2, tc::BK, nt));
-  {
-    const size_t xel = xdtype == SP_BF16 ? 2 : 4;
-    const bool vec = M % 8 == 0 && (size_t(ldx) * xel) % 16 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0;
-    const int per = vec ? 8 : 1;
-    dim3 grid(unsigned(std::min<int64_t>((M / per + 255) / 256, 16)), unsigned(T));
-    tc::gather_rows_bf16_kernel<<<grid, 256, 0, s>>>(x, xdtype, ldx, dev_ids, t0, T, int(M), w.x_tc, L->ldm,
-                                                     vec ? 1 : 0);
-    SP_CUDA(cudaGetLastError());
-    ++C->launches;
-  }
-  const int stage = 2 * tc::BM * tc::BK * 2 + nt * tc::BK * 2;
-  g.stages = std::max(2, std::min(8, (kSmemLimit - 1024 - 256) / stage));
-  const size_t smem = size_t(g.stages) * stage + 1024 + 256;
-  switch (nt) {
-    case 16: SP_CUDA(launch_k(tc::expert_tc_kernel<16>, dim3(g.G), dim3(tc::kFusedThreads), smem, s, true, tw1, tw3, tx, tw2, ta, g)); break;
-    case 32: SP_CUDA(launch_k(tc::expert_tc_kernel<32>, dim3(g.G), dim3(tc::kFusedThreads), smem, s, true, tw1, tw3, tx, tw2, ta, g)); break;
-    case 64: SP_CUDA(launch_k(tc::expert_tc_kernel<64>, dim3(g.G), dim3(tc::kFusedThreads), smem, s, true, tw1, tw3, tx, tw2, ta, g)); break;
-    default: SP_CUDA(launch_k(tc::expert_tc_kernel<128>, dim3(g.G), dim3(tc::kFusedThreads), smem, s, true, tw1, tw3, tx, tw2, ta, g)); break;
-  }
-  ++C->launches;
-  return SP_OK;
-}
-
 // up GEMM (fused SwiGLU / act) into a_tc, then down GEMM accumulated into the call's tc slice.
 // Every workspace is sized and every memset enqueued first, so the chain
 // gather -> up -> (swiglu_reduce) -> down is back-to-back kernels on `s` and
@@ -920,7 +810,6 @@ static int run_block_fused(Context* C, const sp_layer* L, const BlockView& b, co
 static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const void* x, int xdtype, int64_t ldx,
                         CallWs& w, const int32_t* dev_ids, int64_t T_e, int t0, int T, cudaStream_t s,
                         bool resident) {
-  if (use_fused(L, T, resident)) return run_block_fused(C, L, b, x, xdtype, ldx, w, dev_ids, T_e, t0, T, s);
   const int64_t M = L->d.model_dim, N = L->d.out_dim, R = b.rows;
   if (w.tc_slice < 0) {
     w.tc_slice = w.S++;

@@ -1,16 +1,12 @@
-"""GPU parity of the persistent whole-block tcgen05 kernel (expert_tc_kernel,
-csrc/expert_tc.cuh): HBM-resident blocks at 16 < T <= 128 tokens run up GEMM +
-act/gate + down GEMM in one launch with stream-K split tiles and fixed-order
-fix-ups.  Checked against the fp64 oracle on the same bf16 values (north-star
-bf16 bound 1e-2, max |got - ref| / max |ref|), the forward being matched being
-the reference's sliced MLP (slicing_kernel.py:97-124).
-
-Shapes are chosen to hit the kernel's edges: row counts that are not multiples
-of the 128-row tile or the 64-row k-block, output widths that are not multiples
-of the 256-column down tile, model widths that are not multiples of 64, token
-counts on and off the 16/32/64/128 tiles, tiles split over 1..3 CTAs, blocks with
-fewer down units than CTAs (idle CTAs in a phase), and the n_g split (a resident block applied to
-a token sub-range, the other rows of its output slice zero)."""
+"""GPU parity of the tensor-core prefill path (gather -> tcgen05 up GEMM with
+fused SwiGLU -> down GEMM -> finalize) at 5 <= T <= 128 tokens on edge shapes:
+row counts that are not multiples of the 128-row tile or the 64-row k-block,
+output widths that are not multiples of the 256-column down tile, model widths
+that are not multiples of 64, token counts on and off the 16/32/64/128 tiles,
+split-K over many CTAs and over one, and the n_g split (CC rows streamed for the
+diverted prompt rows).  Checked against the fp64 oracle on the same bf16 values
+(north-star bf16 bound 1e-2, max |got - ref| / max |ref|); the forward being
+matched is the reference's sliced MLP (slicing_kernel.py:97-124)."""
 
 from __future__ import annotations
 
@@ -50,8 +46,8 @@ CASES = [
     (200, 700, 260, 64, False, "gelu"),
     (1024, 3000, 1024, 100, True, "silu"),
     (768, 1100, 768, 128, True, "silu"),
-    (128, 130, 68, 20, True, "identity"),  # 2 row tiles, 3 down k-blocks: one CTA
-    (4096, 1000, 64, 24, True, "silu"),  # 16 down units over ~33 CTAs: idle CTAs in the down phase
+    (128, 130, 68, 20, True, "identity"),  # 2 row tiles, 3 down k-blocks
+    (4096, 1000, 64, 24, True, "silu"),  # one 64-column down tile over a long K
     (2048, 5632, 2048, 48, True, "silu"),
 ]
 
@@ -65,9 +61,9 @@ def test_resident_block_matches_oracle(sp, torch, M, H, N, T, gated, act):
     got = sp.mlp_forward_sliced(x, sliced, sp.Activation(act))
     ref = orc.dense_forward(x, w1, w2, act, w3 if gated else None)
     err = orc.max_rel_error(got, ref)
-    print(f"PARITY expert_tc M={M} H={H} N={N} T={T} gated={gated} {act}: {err:.2e}")
+    print(f"PARITY tc M={M} H={H} N={N} T={T} gated={gated} {act}: {err:.2e}")
     assert err <= BF16_TOL
-    # fixed partition and fixed-order fix-ups: bit-identical on repeat
+    # fixed split-K partition, splits summed in order: bit-identical on repeat
     assert np.array_equal(got, sp.mlp_forward_sliced(x, sliced, sp.Activation(act)))
 
 
@@ -89,8 +85,8 @@ def test_split_rates_and_diverted_rows(sp, torch, T, n_g):
 @pytest.mark.slow
 @pytest.mark.parametrize("T", [16, 64, 128])
 def test_full_mixtral_expert(sp, torch, T):
-    """A whole Mixtral-8x7B expert (4096 x 14336 SwiGLU) resident: 112 up tiles
-    and 16 down tiles over every SM; fp64 oracle on a token subset."""
+    """A whole Mixtral-8x7B expert (4096 x 14336 SwiGLU) resident at the
+    per-expert token counts of a 512-token prompt; fp64 oracle on a token subset."""
     from paper_2411_15715_b200.sliced import SlicedFFN
 
     M, H = 4096, 14336
@@ -106,5 +102,5 @@ def test_full_mixtral_expert(sp, torch, T):
     f = lambda t: t.float().cpu().numpy().astype(np.float64)  # noqa: E731
     ref = orc.dense_forward(f(x)[rows], f(w1t).T, f(w2t).T, "silu", f(w3t).T)
     err = orc.max_rel_error(y.float().cpu().numpy()[rows], ref)
-    print(f"PARITY expert_tc mixtral T={T}: {err:.2e}")
+    print(f"PARITY tc mixtral T={T}: {err:.2e}")
     assert err <= BF16_TOL
