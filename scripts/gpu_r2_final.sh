@@ -5,7 +5,7 @@
 # BASELINE config.
 mkdir -p gpurun_out/final/cfg
 F=gpurun_out/final
-timeout 1200 python -m pytest tests -q -m gpu -p no:cacheprovider > $F/gputest.log 2>&1; echo "tests rc=$?" >> $F/gputest.log; tail -3 $F/gputest.log
+timeout 1500 python -m pytest tests -q -m gpu -s -p no:cacheprovider > $F/gputest.log 2>&1; echo "tests rc=$?" >> $F/gputest.log; grep -E "passed|failed|rc=" $F/gputest.log | tail -3
 for i in 1 2; do timeout 600 python bench.py > $F/bench_cfg2_$i.json 2> $F/bench_cfg2_$i.err; done
 timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > $F/bench_reference.json 2> $F/bench_reference.err
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
