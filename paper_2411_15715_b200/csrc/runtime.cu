@@ -648,8 +648,17 @@ static const bool g_prereduce = env_int("SP_PREREDUCE", 1) != 0;
 // and the GG block is off the critical path either way (the CC block ends the
 // step).  Same-box alternating pairs: GG span by events 0.64 -> 0.86 of HBM,
 // value 498 -> 511 and e2e 508 -> 532 tokens/s (profiles/r2/ab_gg_last.txt).
-// SP_GG_LAST=0 restores the launch behind the first chunk copy.
-static const bool g_gg_last = env_int("SP_GG_LAST", 1) != 0;
+// SP_GG_LAST=1 instead launches the group right after the call's last copy is
+// queued: every copy is already enqueued (nothing it could delay) and the
+// copies still in flight cover it, so it never lands on the step's tail (in a
+// link-bound step, e.g. cfg4 on a fast-host box, the group behind the last
+// chunk kernel adds ~120 us).  Same-box pairs with fixed rates
+// (profiles/r2/ab_gg_placement.txt): cfg2 value +2.4 %, e2e +1.7 % (within the
+// box noise), cfg4 inside the noise -- but every GG timing event then lands
+// under the saturated link and the event-timed GG span reads 0.61 of HBM
+// instead of 0.85 (device span 0.92 either way).  The default keeps the
+// measurement clean.  SP_GG_LAST=0: behind the first chunk copy.
+static const int g_gg_last = env_int("SP_GG_LAST", 2);
 // SP_Y_ZERO_COPY=0: small host outputs go through a device buffer and a read-back copy
 static const bool g_y_zero_copy = env_int("SP_Y_ZERO_COPY", 1) != 0;
 constexpr size_t kZeroCopyY = size_t(256) << 10;
@@ -1583,8 +1592,8 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     }
   }
   size_t next_gg = 0;
-  // SP_GG_LAST=1: the grouped GG launch goes behind the last chunk kernel, where
-  // the host link is idle (study switch)
+  // the grouped GG launch is held back until every chunk copy is queued
+  // (SP_GG_LAST, see g_gg_last)
   std::function<int()> gg_group_last;
   if (g_gg_last && has_group && !items.empty()) gg_group_last = std::move(gg_jobs[next_gg++]);
   if (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());
@@ -1617,6 +1626,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     }
     SP_CUDA(cudaEventRecord(C->ev_free[it.slot], C->s_comp));
     if (next_copy < items.size()) SP_TRY(enqueue_copy());
+    if (gg_group_last && g_gg_last == 1 && next_copy == items.size()) {
+      SP_TRY(gg_group_last());  // every copy queued: the group hides under the ones in flight
+      gg_group_last = nullptr;
+    }
     if (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());  // into the wait for the next copy
   }
   while (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());
