@@ -125,3 +125,41 @@ def test_reference_api_layer_cache_is_keyed_by_device(torch):
     assert len(sliced._placed) == 1 and next(iter(sliced._placed))[1] == 0
     with pytest.raises(ValueError, match="cuda:1"):
         sliced.placed(sp.Activation.SILU, device=1)
+
+
+_ORDERING_PROBE = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import torch
+from paper_2411_15715_b200 import _native
+_native.init(0)
+from paper_2411_15715_b200.sliced import SlicedFFN, SlicedMoE
+from oracle import sliced_forward as orc
+rng = np.random.default_rng(21)
+E, M, H = 4, 256, 1024
+ws = [tuple(rng.standard_normal(s).astype(np.float32) / 8 for s in ((H, M), (H, M), (M, H))) for _ in range(E)]
+experts = [SlicedFFN(a, c, None, w3t=b, dtype="bf16", boundaries=(300, 600), chunk_rows=64) for a, b, c in ws]
+router = rng.standard_normal((M, E)).astype(np.float32).astype(np.float64)  # the layer routes with an fp32 router
+moe = SlicedMoE(experts, router, 2)
+q = orc.bf16_round
+for T in (1, 3, 24):
+    x = q(rng.standard_normal((T, M)).astype(np.float32))
+    ref = orc.moe_forward(x, [(q(a.T), q(b.T), q(c.T)) for a, b, c in ws], router, 2)
+    for y in (np.asarray(moe(x)), moe(torch.from_numpy(x.astype(np.float32)).cuda()).float().cpu().numpy()):
+        e = orc.max_rel_error(y, ref)
+        assert e <= 1e-2, (T, e)
+print("OK")
+"""
+
+
+@pytest.mark.parametrize("env", [{"SP_GG_LAST": "0"}, {"SP_GG_LAST": "1"}, {"SP_CC_FIRST": "0"},
+                                 {"SP_CC_BATCH": "0"}, {"SP_PREREDUCE": "0"}, {"SP_TC_PDL": "0"}])
+def test_step_ordering_switches_keep_results(env):
+    """The step-ordering switches (GG group behind the first copy / after the last
+    copy is queued, CC block after the copies, per-call CC passes, no early
+    slice reduction, no PDL in the prefill chain) change only when work runs:
+    an MoE layer with CC + CG + GG blocks still matches the oracle, host and
+    device I/O, decode and tensor-core token counts."""
+    r = subprocess.run([sys.executable, "-c", _ORDERING_PROBE, str(ROOT)], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
