@@ -254,24 +254,34 @@ AMX_TARGET void up_worker(const AmxShared& S) {
         }
         const uint16_t* xg0 = S.xp + size_t(g0 * KP * 32);
         const uint16_t* xg1 = S.xp + size_t((g0 + 1) * KP * 32);
+        // Tile registers are not renamed: a load into a tile waits for every
+        // product still reading it.  So the loop is software pipelined -- each
+        // tile of the NEXT k step is loaded right after its last reader in this
+        // step (W1 after its two products, x0 after the W3 x0 product, x1 and W3
+        // at the end), and those loads run under the remaining products instead
+        // of in front of the next step's.  The weight rows are also prefetched
+        // ahead (first token-group pass only; later passes find them in L2).
+        TLOAD(0, w1 + kc * 2, ldm_b);
+        if (p.gated) TLOAD(1, w3 + kc * 2, ldm_b);
+        TLOAD(2, xg0 + (kc / 2) * 32, 64);
+        if (two) TLOAD(3, xg1 + (kc / 2) * 32, 64);
         for (int64_t k = kc; k < ke; k += 32) {
-          // tile registers are not renamed: a load waits for the products reading
-          // the same tile, so the weight rows are prefetched ahead (first pass
-          // only; later token-group passes find them in L2)
+          const int64_t kn = k + 32;
+          const bool nx = kn < ke;
           if (g0 == 0)
             for (int i = 0; i < 16; ++i) {
               _mm_prefetch(w1 + i * ldm_b + k * 2 + kUpPf, _MM_HINT_T0);
               if (p.gated) _mm_prefetch(w3 + i * ldm_b + k * 2 + kUpPf, _MM_HINT_T0);
             }
-          TLOAD(0, w1 + k * 2, ldm_b);
-          if (p.gated) TLOAD(1, w3 + k * 2, ldm_b);
-          TLOAD(2, xg0 + (k / 2) * 32, 64);
           TDP(4, 0, 2);
+          if (two) TDP(5, 0, 3);
+          if (nx) TLOAD(0, w1 + kn * 2, ldm_b);
           if (p.gated) TDP(6, 1, 2);
-          if (two) {
-            TLOAD(3, xg1 + (k / 2) * 32, 64);
-            TDP(5, 0, 3);
-            if (p.gated) TDP(7, 1, 3);
+          if (nx) TLOAD(2, xg0 + (kn / 2) * 32, 64);
+          if (p.gated && two) TDP(7, 1, 3);
+          if (nx) {
+            if (two) TLOAD(3, xg1 + (kn / 2) * 32, 64);
+            if (p.gated) TLOAD(1, w3 + kn * 2, ldm_b);
           }
         }
         TSTORE(4, zc, 64);
@@ -384,18 +394,25 @@ AMX_TARGET void down_worker(const AmxShared& S, std::atomic<int64_t>* rounds, in
             if (g2 && j2) TLOAD(3, y0 + 16 * nr + 16, nr * 4);
           }
           const uint16_t* b0 = w2p + jn * 32;
-          for (int64_t sl = kc / 32; sl < ke / 32; ++sl) {
-            TLOAD(4, a0 + 32 * sl, b1p * 2);
-            TLOAD(6, b0 + (16 * sl) * nr * 2, nr * 4);
+          // software pipelined like the up loop: each tile of the next hidden
+          // step is loaded right after its last reader in this one
+          const int64_t s0 = kc / 32, se = ke / 32;
+          TLOAD(4, a0 + 32 * s0, b1p * 2);
+          TLOAD(6, b0 + (16 * s0) * nr * 2, nr * 4);
+          if (j2) TLOAD(7, b0 + (16 * s0) * nr * 2 + 32, nr * 4);
+          if (g2) TLOAD(5, a1 + 32 * s0, b1p * 2);
+          for (int64_t sl = s0; sl < se; ++sl) {
+            const int64_t sn = sl + 1;
+            const bool nx = sn < se;
             TDP(0, 4, 6);
-            if (j2) {
-              TLOAD(7, b0 + (16 * sl) * nr * 2 + 32, nr * 4);
-              TDP(1, 4, 7);
-            }
-            if (g2) {
-              TLOAD(5, a1 + 32 * sl, b1p * 2);
-              TDP(2, 5, 6);
-              if (j2) TDP(3, 5, 7);
+            if (j2) TDP(1, 4, 7);
+            if (nx) TLOAD(4, a0 + 32 * sn, b1p * 2);
+            if (g2) TDP(2, 5, 6);
+            if (nx) TLOAD(6, b0 + (16 * sn) * nr * 2, nr * 4);
+            if (g2 && j2) TDP(3, 5, 7);
+            if (nx) {
+              if (j2) TLOAD(7, b0 + (16 * sn) * nr * 2 + 32, nr * 4);
+              if (g2) TLOAD(5, a1 + 32 * sn, b1p * 2);
             }
           }
           TSTORE(0, y0, nr * 4);
