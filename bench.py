@@ -292,6 +292,41 @@ def calibrate_host_terms(args, profile, rates, spans, steps) -> tuple:
     return costs.profile_from_dict(doc), info
 
 
+def calibrate_prompt_terms(profile, layer_spec, rates, plans, layers, spans) -> tuple:
+    """The prompt-phase counterpart of calibrate_host_terms.  ``spans`` are the
+    library trace of one prefill through ``layers`` layers cycling ``plans``:
+    measured host CC busy and copy busy, over what the profile predicts for the
+    same calls (planner.prompt_layer_busy), scale the profile's CPU GEMM and
+    PCIe terms.  The caller re-plans the token split on the result."""
+    import paper_2411_15715_b200 as sp
+    from paper_2411_15715_b200 import costs
+
+    pred_link = pred_cpu = 0.0
+    for l in range(layers):
+        calls = plans[l % len(plans)]
+        lk, cp = sp.prompt_layer_busy(profile, layer_spec, [len(c.token_ids) for c in calls],
+                                      [c.n_g for c in calls], rates)
+        pred_link += lk
+        pred_cpu += cp
+    meas_cpu = sum(s["end_s"] - s["start_s"] for s in spans if s["kind"] == "cc")
+    meas_link = sum(s["end_s"] - s["start_s"] for s in spans if s["kind"] == "copy")
+    k_cpu = meas_cpu / pred_cpu if pred_cpu > 0 and meas_cpu > 0 else 1.0
+    k_link = meas_link / pred_link if pred_link > 0 and meas_link > 0 else 1.0
+    doc = costs.profile_to_dict(profile)
+    for g in doc.get("gemm", {}).values():
+        if "cpu" in g:
+            g["cpu"]["alpha"] *= k_cpu
+            g["cpu"]["beta"] *= k_cpu
+    if "pcie" in doc:
+        doc["pcie"]["alpha"] *= k_link
+        doc["pcie"]["beta"] *= k_link
+    info = {"k_cpu": k_cpu, "k_link": k_link, "layers": layers,
+            "n_g_layer0_before": [c.n_g for c in plans[0]],
+            "cpu_busy_s": {"measured": meas_cpu, "predicted": pred_cpu},
+            "transfer_busy_s": {"measured": meas_link, "predicted": pred_link}}
+    return costs.profile_from_dict(doc), info
+
+
 # ---------------------------------------------------------------------------
 # clocks
 
@@ -874,6 +909,24 @@ def run_prefill_decode(args):
         for l in range(args.layers):
             forward_calls(prompt_plans[l % D], xp, out=out_p)
 
+    # ---- per-box recalibration of the prompt profile's host terms, then re-plan ----
+    pcalib = None
+    if args.calibrate:
+        prefill()  # staging / workspaces at prompt size
+        torch.cuda.synchronize()
+        nat.trace_enable(True)
+        prefill()
+        torch.cuda.synchronize()
+        cspans = nat.trace_fetch()
+        nat.trace_enable(False)
+        p_profile, pcalib = calibrate_prompt_terms(p_profile, layer_spec, rates, prompt_plans, args.layers, cspans)
+        p_source += (f" (host terms recalibrated on this box: CPU x{pcalib['k_cpu']:.3f}, "
+                     f"link x{pcalib['k_link']:.3f})")
+        ng_cache.clear()
+        layer_plans.clear()
+        prompt_plans = [plan(d, xp_host, True) for d in range(D)]
+        pcalib["n_g_layer0_after"] = [c.n_g for c in prompt_plans[0]]
+
     def decode():
         for i in range(args.decode_steps):
             for l in range(args.layers):
@@ -950,7 +1003,7 @@ def run_prefill_decode(args):
                    "l2": f"{D} distinct layers x 8 experts ({D * 2.8:.0f} GB) cycled, >> L2"},
         "e2e": {"value": args.prompt / t_e2e, "unit": UNIT, "h2d_bytes_per_step": args.prompt * args.model_dim * 2 * args.layers,
                 "d2h_bytes_per_step": args.prompt * args.model_dim * 4 * args.layers},
-        "gpu_launches": launches, "clocks": clk.summary(),
+        "gpu_launches": launches, "clocks": clk.summary(), "prompt_calibration": pcalib,
         "ycc_transfer": {"measured_ms_per_layer": ycc_meas * 1e3,
                          "model_ms_per_layer": ycc_model * 1e3 if ycc_model is not None else None,
                          "note": "CC partials host->HBM (pipeline.py:367-383 cc_result_transfer_time, fp32 "

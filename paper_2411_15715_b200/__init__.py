@@ -57,6 +57,7 @@ from .planner import (
     prompt_speedup,
     solve_ng,
     solve_ng_layer,
+    prompt_layer_busy,
     solve_rates_grid,
     solve_rcg,
 )

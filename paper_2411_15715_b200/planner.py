@@ -360,6 +360,39 @@ class LayerTokenPlan:
     cpu_s: float               # modelled host CC time of the layer
 
 
+def _prompt_call_costs(profile: HardwareProfile, layer: LayerSpec, rates: SlicingRates, chunk_bytes: float):
+    """(link(T_e, n_g), cpu(T_e, n_g)) seconds of one expert call in the prompt
+    phase: the linear model solve_ng_layer plans with (docstring there)."""
+    gemm, pcie = profile.gemm[layer.precision], profile.require_pcie()
+    G = float(layer.n_gemms)
+    W = float(layer.weight_bytes)
+    mh = float(layer.model_dim) * layer.hidden_dim
+    cc, cg = rates.cc, rates.cg
+
+    def link(t: int, ng: int) -> float:
+        nbytes = (cg + (cc if ng > 0 else 0.0)) * G * W
+        return pcie.alpha * math.ceil(nbytes / chunk_bytes) + nbytes * pcie.beta if nbytes > 0 else 0.0
+
+    def cpu(t: int, ng: int) -> float:
+        kept = t - ng
+        return G * (gemm.cpu.alpha + kept * cc * mh * gemm.cpu.beta) if kept > 0 and cc > 0 else 0.0
+
+    return link, cpu
+
+
+def prompt_layer_busy(
+    profile: HardwareProfile, layer: LayerSpec, tokens: Sequence[int], n_g: Sequence[int], rates: SlicingRates,
+    chunk_bytes: float = 8 << 20,
+) -> tuple[float, float]:
+    """EXTENSION: predicted (link busy, host CC busy) seconds of one MoE layer's
+    prompt calls with the given per-expert splits -- any plan's, solve_ng's or
+    solve_ng_layer's -- under solve_ng_layer's cost model.  Used to re-anchor
+    the prompt profile on a box from a traced prefill."""
+    link, cpu = _prompt_call_costs(profile, layer, rates, chunk_bytes)
+    return (sum(link(int(t), int(n)) for t, n in zip(tokens, n_g)),
+            sum(cpu(int(t), int(n)) for t, n in zip(tokens, n_g)))
+
+
 def solve_ng_layer(
     profile: HardwareProfile, layer: LayerSpec, tokens: Sequence[int], rates: SlicingRates,
     chunk_bytes: float = 8 << 20,
@@ -377,20 +410,7 @@ def solve_ng_layer(
         cpu_e  = G * (alpha_C + (T_e - n_g) * cc * M * H * beta_C)
     (G GEMMs per expert = layer.n_gemms, W = layer.weight_bytes).  Ties go to
     the lower expert index; deterministic."""
-    gemm, pcie = profile.gemm[layer.precision], profile.require_pcie()
-    G = float(layer.n_gemms)
-    W = float(layer.weight_bytes)
-    mh = float(layer.model_dim) * layer.hidden_dim
-    cc, cg = rates.cc, rates.cg
-
-    def link(t: int, ng: int) -> float:
-        nbytes = (cg + (cc if ng > 0 else 0.0)) * G * W
-        return pcie.alpha * math.ceil(nbytes / chunk_bytes) + nbytes * pcie.beta if nbytes > 0 else 0.0
-
-    def cpu(t: int, ng: int) -> float:
-        kept = t - ng
-        return G * (gemm.cpu.alpha + kept * cc * mh * gemm.cpu.beta) if kept > 0 and cc > 0 else 0.0
-
+    link, cpu = _prompt_call_costs(profile, layer, rates, chunk_bytes)
     ng = [int(t) for t in tokens]  # start: every row on the GPU
 
     def layer_time(plan):
