@@ -199,3 +199,28 @@ def test_solve_ng_layer_extension_limits():
     assert ps.n_g == tuple(toks)
     again = sp.solve_ng_layer(costs.profile_from_dict(fast), layer_, toks, rates)
     assert again == pf
+
+
+def test_prompt_layer_busy_matches_the_layer_plan():
+    """planner.prompt_layer_busy (extension: the cost model the bench re-anchors
+    the prompt profile with) reproduces solve_ng_layer's own link / host
+    predictions for the plan it returns, and scales linearly in the CPU terms."""
+    import copy
+
+    from paper_2411_15715_b200 import costs
+
+    base = costs.profile_to_dict(PROFILES[0]) if isinstance(PROFILES, list) else costs.profile_to_dict(
+        next(iter(PROFILES.values())))
+    layer_ = sp.LayerSpec(4096, 14336, n_gemms=3, precision=sp.Precision.FP16)
+    rates = sp.SlicingRates(0.35, 0.15, 0.5)
+    toks = [100, 120, 130, 140, 0, 90]
+    prof = costs.profile_from_dict(base)
+    plan = sp.solve_ng_layer(prof, layer_, toks, rates)
+    lk, cp = sp.prompt_layer_busy(prof, layer_, toks, plan.n_g, rates)
+    assert lk == plan.link_s and cp == plan.cpu_s
+    half = copy.deepcopy(base)
+    for g in half["gemm"].values():
+        g["cpu"]["alpha"] *= 0.5
+        g["cpu"]["beta"] *= 0.5
+    _, cp2 = sp.prompt_layer_busy(costs.profile_from_dict(half), layer_, toks, plan.n_g, rates)
+    assert abs(cp2 - 0.5 * cp) <= 1e-12 * max(1.0, cp)
