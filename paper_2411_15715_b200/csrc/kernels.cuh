@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
   int gi = 0;
   while (gi + 1 < grp.n && int(blockIdx.x) >= grp.a[gi + 1].cta0) ++gi;
   const FfnArgs& p = grp.a[gi];
-  const int cta = int(blockIdx.x) - p.cta0, ncta = p.ncta;
+  const int cta = int(blockIdx.x) - p.cta0;
   constexpr int VE = VecTraits<WT>::kElems;
   constexpr int G = GATED ? 2 : 1;
   constexpr int STEP = 32 * VE;
@@ -231,9 +231,14 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   SP_STAMP(0);
+  if (p.stamps && threadIdx.x == 0) {  // debug: the SM this CTA runs on
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.stamps[blockIdx.x * 8 + 7] = smid;
+  }
   if (p.kspan0 && threadIdx.x == 0) atomicMin(p.kspan0, global_ns());
-  const int64_t r_begin = (int64_t)p.rows * cta / ncta;
-  const int64_t r_end = (int64_t)p.rows * (cta + 1) / ncta;
+  const int64_t r_begin = (int64_t)p.rows * cta / p.ncta;
+  const int64_t r_end = (int64_t)p.rows * (cta + 1) / p.ncta;
   const int n_local = int(r_end - r_begin);
   const int NST = fp.stages;
   const int n_up = (n_local + fp.rs_up - 1) / fp.rs_up;
