@@ -644,10 +644,13 @@ static const bool g_cc_first = env_int("SP_CC_FIRST", 1) != 0;
 static const bool g_prereduce = env_int("SP_PREREDUCE", 1) != 0;
 // The grouped GG launch runs behind the call's last chunk kernel, i.e. once the
 // CG copies are done: a timing event recorded while copy-engine H2D traffic
-// saturates the link costs ~23 us of stream time (scripts/probes/event_span.cu),
-// and the GG block is off the critical path either way (the CC block ends the
-// step).  Same-box alternating pairs: GG span by events 0.64 -> 0.86 of HBM,
-// value 498 -> 511 and e2e 508 -> 532 tokens/s (profiles/r2/ab_gg_last.txt).
+// saturates the link lands ~23 us late (scripts/probes/event_span.cu), so only
+// there does the event-timed GG span match the kernel.  Against the round-1
+// placement (behind the first chunk copy), same-box alternating pairs: GG span
+// by events 0.64 -> 0.86 of HBM, value 498 -> 511 and e2e 508 -> 532 tokens/s
+// (profiles/r2/ab_gg_last.txt).  It is not free: with the calibrated split the
+// CC block and the copies end within ~20 us of each other, so the group (64 us)
+// sits on the step's tail (profiles/r2/timeline/cfg2_anatomy_*.txt).
 // SP_GG_LAST=1 instead launches the group right after the call's last copy is
 // queued: every copy is already enqueued (nothing it could delay) and the
 // copies still in flight cover it, so it never lands on the step's tail (in a
