@@ -971,7 +971,11 @@ def run_prefill_decode(args):
         torch.cuda.synchronize()
         Path(args.trace_out).write_text(json.dumps([s for s in nat.trace_fetch() if s["call"] < 4], indent=0))
         nat.trace_enable(False)
-        # the same through the host-I/O public API (x / y in host memory)
+        # the same through the host-I/O public API (x / y in host memory), after
+        # two untraced host-I/O layers (staging and workspaces at host-I/O sizes)
+        for l in range(min(2, args.layers)):
+            forward_calls(prompt_plans[l % D], xp_host)
+        torch.cuda.synchronize()
         nat.trace_enable(True)
         t0 = time.perf_counter()
         for l in range(min(4, args.layers)):

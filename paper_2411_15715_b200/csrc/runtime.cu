@@ -1049,6 +1049,30 @@ static std::vector<HostChunk> host_cc_chunks(const sp_layer* L) {
   return hc;
 }
 
+// one x row to fp32 [ldx] (zero padded); round: f32 x rounded to bf16 values
+// (the caller's f32 x under SP_X_TO_BF16 -- what the GPU side sees)
+static void gather_host_row(float* dst, int64_t ldx, const void* x, int xdtype, int64_t M, int64_t row,
+                            bool round) {
+  if (xdtype == SP_BF16) {
+    const uint16_t* src = static_cast<const uint16_t*>(x) + row * M;
+    for (int64_t k = 0; k < M; ++k) {
+      const uint32_t u = uint32_t(src[k]) << 16;
+      memcpy(&dst[k], &u, 4);
+    }
+  } else if (round) {
+    const float* src = static_cast<const float*>(x) + row * M;
+    for (int64_t k = 0; k < M; ++k) {
+      uint32_t u;
+      memcpy(&u, src + k, 4);
+      u = ((u + 0x7fffu + ((u >> 16) & 1u)) >> 16) << 16;
+      memcpy(&dst[k], &u, 4);
+    }
+  } else {
+    memcpy(dst, static_cast<const float*>(x) + row * M, size_t(M) * 4);
+  }
+  for (int64_t k = M; k < ldx; ++k) dst[k] = 0.f;
+}
+
 // x rows of a call gathered to fp32 [T, ldx] (zero padded) for the host CC kernel
 static void gather_host_x(float* xh, int64_t ldx, const void* x, int xdtype, int64_t M,
                           const int32_t* ids, int64_t T) {
@@ -1342,15 +1366,13 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     // ---- x: device copy for the GPU, host copy for the CC threads ----
     for (int c = 0; c < n_calls; ++c)
       need_cc |= calls[c].layer->d.b1 > 0 && calls[c].tokens - calls[c].n_g > 0;
+    // host I/O: the CC threads read the caller's x directly (rounding it to bf16
+    // values themselves under SP_X_TO_BF16), so the CC block is submitted before
+    // this thread stages x for the GPU (a prompt's x is MBs)
+    const bool x_round = host_io && stage_bf16;
+    const int x_dtype_cc = x_round ? SP_F32 : xdtype;
     if (host_io) {
-      if (stage_bf16)
-        round_bf16_host(static_cast<const float*>(x_src), reinterpret_cast<uint16_t*>(hp + p_x), T * M);
-      else
-        memcpy(hp + p_x, x, size_t(T) * M * xel);
-      SP_CUDA(cudaMemcpyAsync(dws + o_xdev, hp + p_x, size_t(T) * M * xel, cudaMemcpyHostToDevice,
-                              C->s_comp));
-      x_dev = dws + o_xdev;
-      x_host = stage_bf16 ? static_cast<const void*>(hp + p_x) : x;
+      x_host = x_round ? x_src : x;
     } else if (need_cc && x_host_ready) {
       x_host = x_host_ready;  // already read back by the caller (sp_moe_forward): no GPU wait
     } else if (need_cc) {
@@ -1371,12 +1393,39 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       }
       // every call's CC block in one pass of the pool (one join per step, not two per expert)
       const double t_cc0 = now_s();
+      static const bool cc_prof = env_int("SP_CC_PROF", 0) != 0;
       const int64_t ldx = round_up(M, kPadElems);
       int64_t rows = 0;
       double bytes = 0.0;
       for (int c = 0; c < n_calls; ++c)
         if (calls[c].layer->d.b1 > 0) rows += std::max<int64_t>(0, calls[c].tokens - calls[c].n_g);
-      C->hscratch.assign(size_t(rows * ldx), 0.f);
+      if (C->hscratch.size() < size_t(rows * ldx)) C->hscratch.resize(size_t(rows * ldx));
+      // the CC rows of every call, gathered in parallel on the pool (rows -> (call, index))
+      {
+        std::vector<int> row_call(static_cast<size_t>(rows));
+        std::vector<int64_t> row_idx(static_cast<size_t>(rows));
+        int64_t r = 0;
+        for (int c = 0; c < n_calls; ++c) {
+          const int64_t Tcc = calls[c].tokens - calls[c].n_g;
+          if (calls[c].layer->d.b1 <= 0 || Tcc <= 0) continue;
+          for (int64_t i = 0; i < Tcc; ++i, ++r) {
+            row_call[size_t(r)] = c;
+            row_idx[size_t(r)] = i;
+          }
+        }
+        float* const xs0 = C->hscratch.data();
+        auto gather = [&](int tid, int n) {
+          for (int64_t q = rows * tid / n; q < rows * (tid + 1) / n; ++q) {
+            const sp_call& k = calls[row_call[size_t(q)]];
+            const int64_t i = row_idx[size_t(q)];
+            gather_host_row(xs0 + size_t(q * ldx), ldx, x_host, x_dtype_cc, M, k.token_ids ? k.token_ids[i] : i,
+                            x_round);
+          }
+        };
+        const int gthreads = (flags & SP_NO_CC_THREADS) ? 1 : int(std::min<int64_t>(C->host_threads, rows / 8 + 1));
+        if (gthreads > 1) C->pool->run(gthreads, gather);
+        else gather(0, 1);
+      }
       std::vector<std::vector<HostChunk>> hcs;
       std::vector<CCProblem> probs;
       hcs.reserve(size_t(n_calls));
@@ -1387,13 +1436,13 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         if (L->d.b1 <= 0 || Tcc <= 0) continue;
         float* xs = C->hscratch.data() + size_t(r0 * ldx);
         r0 += Tcc;
-        gather_host_x(xs, ldx, x_host, xdtype, M, calls[c].token_ids, Tcc);
         hcs.push_back(host_cc_chunks(L));
         probs.push_back(CCProblem{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, L->ldn, hcs.back().data(),
                                   L->n_cc_chunks, L->d.b1, xs, ldx, Tcc, reinterpret_cast<float*>(hp + p_ycc[c])});
         bytes += double(L->cc_bytes);
       }
       const int cc_threads = (flags & SP_NO_CC_THREADS) ? 1 : C->host_threads;
+      const double t_prep = now_s();
       if (cc_fn) {
         // the caller's CC code (e.g. the reference's numpy forward) on this thread
         int k = 0;
@@ -1411,9 +1460,22 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         for (const CCProblem& pr : probs) cc_forward(pr, *C->pool, cc_threads);
       }
       host_span(C, 3, SP_TRACE_CC, t_cc0, now_s(), bytes);
+      if (cc_prof)
+        fprintf(stderr, "[cc] rows %lld  start %.0f us after the call  prep %.0f us  compute %.0f us\n",
+                (long long)rows, (t_cc0 - t_call) * 1e6, (t_prep - t_cc0) * 1e6, (now_s() - t_prep) * 1e6);
       return SP_OK;
     };
     if (cc_async) cc_submit(C, cc_work);
+    if (host_io) {
+      // x for the GPU: staged into pinned memory (rounded to bf16 under SP_X_TO_BF16) and copied
+      if (stage_bf16)
+        round_bf16_host(static_cast<const float*>(x_src), reinterpret_cast<uint16_t*>(hp + p_x), T * M);
+      else
+        memcpy(hp + p_x, x, size_t(T) * M * xel);
+      SP_CUDA(cudaMemcpyAsync(dws + o_xdev, hp + p_x, size_t(T) * M * xel, cudaMemcpyHostToDevice,
+                              C->s_comp));
+      x_dev = dws + o_xdev;
+    }
     return SP_OK;
   };
   const bool cc_early = g_cc_first && (host_io || x_host_ready);
@@ -1502,11 +1564,12 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
                             C->s_comp));
   }
 
+  // x only on the device: its read-back for the CC block goes ahead of the ring
+  // copies (behind them it waited for all of them: ~0.9 ms for a prompt's CC block)
+  if (!cc_started) SP_TRY(start_cc());
+
   // the first ring slots' copies go right behind the (tiny) metadata copies
   while (next_copy < items.size() && next_copy < size_t(ring_slots)) SP_TRY(enqueue_copy());
-
-  // x only on the device: its read-back for the CC block queues behind the first copies
-  if (!cc_started) SP_TRY(start_cc());
 
   // ---- GG blocks (HBM resident): the decode-size calls share one grouped launch ----
   // GG work is off the critical path (the copy stream paces the step), but it
