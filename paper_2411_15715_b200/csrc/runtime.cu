@@ -1466,16 +1466,21 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       return SP_OK;
     };
     if (cc_async) cc_submit(C, cc_work);
-    if (host_io) {
-      // x for the GPU: staged into pinned memory (rounded to bf16 under SP_X_TO_BF16) and copied
-      if (stage_bf16)
-        round_bf16_host(static_cast<const float*>(x_src), reinterpret_cast<uint16_t*>(hp + p_x), T * M);
-      else
-        memcpy(hp + p_x, x, size_t(T) * M * xel);
-      SP_CUDA(cudaMemcpyAsync(dws + o_xdev, hp + p_x, size_t(T) * M * xel, cudaMemcpyHostToDevice,
-                              C->s_comp));
-      x_dev = dws + o_xdev;
-    }
+    return SP_OK;
+  };
+  // host I/O: x for the GPU, staged into pinned memory (rounded to bf16 under
+  // SP_X_TO_BF16) and copied.  Done once the ring's first chunk copies are
+  // queued: a prompt's x is MBs, and staging it first kept the link idle ~1 ms.
+  bool x_dev_staged = !host_io;
+  auto stage_x_dev = [&]() -> int {
+    if (x_dev_staged) return SP_OK;
+    x_dev_staged = true;
+    if (stage_bf16)
+      round_bf16_host(static_cast<const float*>(x_src), reinterpret_cast<uint16_t*>(hp + p_x), T * M);
+    else
+      memcpy(hp + p_x, x, size_t(T) * M * xel);
+    SP_CUDA(cudaMemcpyAsync(dws + o_xdev, hp + p_x, size_t(T) * M * xel, cudaMemcpyHostToDevice, C->s_comp));
+    x_dev = dws + o_xdev;
     return SP_OK;
   };
   const bool cc_early = g_cc_first && (host_io || x_host_ready);
@@ -1570,6 +1575,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
 
   // the first ring slots' copies go right behind the (tiny) metadata copies
   while (next_copy < items.size() && next_copy < size_t(ring_slots)) SP_TRY(enqueue_copy());
+  SP_TRY(stage_x_dev());
 
   // ---- GG blocks (HBM resident): the decode-size calls share one grouped launch ----
   // GG work is off the critical path (the copy stream paces the step), but it
