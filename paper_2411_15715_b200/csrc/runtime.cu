@@ -1806,7 +1806,19 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   drain.armed = false;
   if (host_io) {
     SP_CUDA(cudaStreamSynchronize(C->s_comp));
-    memcpy(y, hp + p_y, size_t(T) * N * yel);
+    // a prompt's output is MBs, usually into a fresh (not yet faulted-in) array:
+    // copy it out on the pool, in 64 KB-aligned shares
+    const size_t ybytes = size_t(T) * N * yel;
+    const int nt = ybytes >= (size_t(1) << 20) ? C->pool->size() : 1;
+    if (nt > 1) {
+      C->pool->run(nt, [&](int tid, int n) {
+        const size_t a = (ybytes * size_t(tid) / size_t(n)) & ~size_t(65535);
+        const size_t b = tid + 1 == n ? ybytes : (ybytes * size_t(tid + 1) / size_t(n)) & ~size_t(65535);
+        if (b > a) memcpy(static_cast<char*>(y) + a, hp + p_y + a, b - a);
+      });
+    } else {
+      memcpy(y, hp + p_y, ybytes);
+    }
   } else {
     SP_CUDA(cudaStreamWaitEvent(user, C->ev_done, 0));
   }

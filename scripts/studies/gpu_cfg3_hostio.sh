@@ -1,11 +1,8 @@
 #!/bin/bash
-# cfg3 host-I/O layer anatomy with the x staging deferred behind the first ring copies, then
-# ring depth for long streams 6 vs 8 (cfg3 layer plan, calibrated), alternating
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_tc_shapes.py -q -m gpu -p no:cacheprovider 2>&1 | tail -1
-bash scripts/studies/gpu_cfg3_trace.sh 2>&1 | grep -E "wall|== host|copy_start|cc_start|period" | tail -5
+# cfg3 host-I/O: parity of the host-I/O paths, the host-I/O layer anatomy, then cfg3 (layer plan, calibrated) twice
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_tc_shapes.py tests/test_config_parity.py -q -m gpu -p no:cacheprovider 2>&1 | tail -1
+bash scripts/studies/gpu_cfg3_trace.sh 2>&1 | grep -E "wall|== host|copy_start|cc_start|merge_end|return_end|period" | tail -7
 for r in 1 2; do
-  for v in 6 8; do
-    SP_RING_SLOTS_LONG=$v timeout 900 python bench.py --config cfg3 --layers 32 --distinct-layers 4 --decode-steps 8 --token-plan layer 2>/dev/null | grep '^{' | tail -1 | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print('ring $v', round(d['value'],1), 'e2e', round(d['e2e']['value'],1))"
-  done
+  timeout 900 python bench.py --config cfg3 --layers 32 --distinct-layers 4 --decode-steps 8 --token-plan layer 2>/dev/null | grep '^{' | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('cfg3', round(d['value'],1), 'e2e', round(d['e2e']['value'],1))"
 done
