@@ -664,6 +664,7 @@ static const bool g_prereduce = env_int("SP_PREREDUCE", 1) != 0;
 static const int g_gg_last = env_int("SP_GG_LAST", 2);
 // SP_Y_ZERO_COPY=0: small host outputs go through a device buffer and a read-back copy
 static const bool g_y_zero_copy = env_int("SP_Y_ZERO_COPY", 1) != 0;
+static const bool g_host_merge = env_int("SP_HOST_MERGE", 1) != 0;
 constexpr size_t kZeroCopyY = size_t(256) << 10;
 constexpr int kTcMaxSplits = 24;
 // finalize: per-token rows kernel up to this many slices per call, slice groups beyond
@@ -1376,8 +1377,12 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     } else if (need_cc && x_host_ready) {
       x_host = x_host_ready;  // already read back by the caller (sp_moe_forward): no GPU wait
     } else if (need_cc) {
-      SP_CUDA(cudaMemcpyAsync(hp + p_x, x, size_t(T) * M * xel, cudaMemcpyDeviceToHost, C->s_comp));
-      SP_CUDA(cudaEventRecord(C->ev_x, C->s_comp));
+      // on the aux stream, ordered after the caller's work only: on the compute
+      // stream it also waited for the previous forward's GPU tail, so
+      // back-to-back prompt layers could not start their CC blocks early
+      SP_CUDA(cudaStreamWaitEvent(C->s_aux, C->ev_user, 0));
+      SP_CUDA(cudaMemcpyAsync(hp + p_x, x, size_t(T) * M * xel, cudaMemcpyDeviceToHost, C->s_aux));
+      SP_CUDA(cudaEventRecord(C->ev_x, C->s_aux));
       x_host = hp + p_x;
     }
 
@@ -1728,13 +1733,20 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     fa.entry_gate = reinterpret_cast<const float*>(fa.entry_row + total_rows);
   }
   bool ycc_copy = false;
+  // Host I/O with an output too big for the zero-copy path (a prompt): the CC
+  // partials are added on the host to the read-back device output, so the GPU
+  // finalize and the read-back run before the CC block ends and its MBs of
+  // partials never cross the link (SP_HOST_MERGE=0: through the GPU finalize)
+  const bool host_merge = g_host_merge && host_io && !y_zero_copy && ydtype == SP_F32 && need_cc && cc_async;
   for (int c = 0; c < n_calls; ++c) {
     const sp_layer* L = calls[c].layer;
     const int64_t Tcc = calls[c].tokens - calls[c].n_g;
     const bool has_cc = L->d.b1 > 0 && Tcc > 0;
     const bool zc = size_t(Tcc) * N * 4 <= kZeroCopyYcc;
-    ycc_copy |= has_cc && !zc;
-    const float* ycc = !has_cc ? nullptr : zc ? reinterpret_cast<const float*>(hp + p_ycc[c]) : ws[c].ycc;
+    if (!host_merge) ycc_copy |= has_cc && !zc;
+    const float* ycc = (!has_cc || host_merge) ? nullptr
+                       : zc ? reinterpret_cast<const float*>(hp + p_ycc[c])
+                            : ws[c].ycc;
     fa.c[c] = FinalCall{ws[c].part, ws[c].S, ycc, int(Tcc), int(calls[c].tokens)};
   }
   // The finalize waits for the host CC block: reduce the device partial slices
@@ -1797,7 +1809,10 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     return SP_OK;
   };
   C->hpin_used[hb] = true;  // from here on the half's last GPU use is behind hpin_done[hb]
-  if (need_cc && cc_async) {
+  if (need_cc && cc_async && host_merge) {
+    SP_TRY(tail());  // the GPU finalize without the CC partials and the read-back, now
+    SP_TRY(cc_join_with_tail(C, [] { return SP_OK; }));
+  } else if (need_cc && cc_async) {
     SP_TRY(cc_join_with_tail(C, tail));
   } else {
     if (need_cc) SP_TRY(cc_work());
@@ -1810,7 +1825,32 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     // copy it out on the pool, in 64 KB-aligned shares
     const size_t ybytes = size_t(T) * N * yel;
     const int nt = ybytes >= (size_t(1) << 20) ? C->pool->size() : 1;
-    if (nt > 1) {
+    if (host_merge) {
+      // y[t] = device part[t] + sum over t's entries (call c, row i, gate) with a CC
+      // row of gate * y_cc_c[i], entries in the host CSR's order
+      const double t_m0 = now_s();
+      const int32_t* cs = reinterpret_cast<const int32_t*>(hp + p_csr);
+      const int32_t* ecall = cs + (T + 1);
+      const int32_t* erow = ecall + total_rows;
+      const float* egate = reinterpret_cast<const float*>(erow + total_rows);
+      const float* ydev = reinterpret_cast<const float*>(hp + p_y);
+      float* yout = static_cast<float*>(y);
+      C->pool->run(nt, [&](int tid, int n) {
+        for (int64_t t = T * tid / n; t < T * (tid + 1) / n; ++t) {
+          float* dst = yout + t * N;
+          memcpy(dst, ydev + t * N, size_t(N) * 4);
+          for (int32_t e = cs[t]; e < cs[t + 1]; ++e) {
+            const int c = ecall[e];
+            const int64_t i = erow[e];
+            if (calls[c].layer->d.b1 <= 0 || i >= calls[c].tokens - calls[c].n_g) continue;
+            const float g = egate[e];
+            const float* yc = reinterpret_cast<const float*>(hp + p_ycc[c]) + i * N;
+            for (int64_t k = 0; k < N; ++k) dst[k] += g * yc[k];
+          }
+        }
+      });
+      host_span(C, 3, SP_TRACE_MERGE, t_m0, now_s(), double(ybytes));
+    } else if (nt > 1) {
       C->pool->run(nt, [&](int tid, int n) {
         const size_t a = (ybytes * size_t(tid) / size_t(n)) & ~size_t(65535);
         const size_t b = tid + 1 == n ? ybytes : (ybytes * size_t(tid + 1) / size_t(n)) & ~size_t(65535);

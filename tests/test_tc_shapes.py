@@ -104,3 +104,29 @@ def test_full_mixtral_expert(sp, torch, T):
     err = orc.max_rel_error(y.float().cpu().numpy()[rows], ref)
     print(f"PARITY tc mixtral T={T}: {err:.2e}")
     assert err <= BF16_TOL
+
+
+@pytest.mark.parametrize("n_g", [0, 70])
+def test_host_io_prompt_merges_cc_on_the_host(sp, torch, n_g):
+    """Host-I/O prompt calls whose output exceeds the zero-copy limit add the CC
+    partials on the host to the read-back device output (SP_HOST_MERGE): a dense
+    layer with CC + CG + GG blocks and the n_g split, and a top-2 MoE layer
+    (gates, several calls per token) -- both against the oracle."""
+    from paper_2411_15715_b200.sliced import SlicedFFN, SlicedMoE
+
+    rng = np.random.default_rng(900 + n_g)
+    q = orc.bf16_round
+    T, M, H = 200, 1024, 1536
+    x, w1, w3, w2 = (q(rng.standard_normal(s) / d) for s, d in (((T, M), 1), ((M, H), 16), ((M, H), 16), ((H, M), 16)))
+    sliced = sp.slice_weights(w1, w2, sp.SlicingRates(0.3, 0.3, 0.4), w3, dtype="bf16", chunk_rows=256)
+    got = sp.mlp_forward_sliced(x, sliced, sp.Activation.SILU, n_g)  # numpy x: host I/O, 800 KB output
+    ref = orc.sliced_forward(x, w1, w2, "silu", 0.3, 0.3, w3)
+    assert orc.max_rel_error(got, ref) <= BF16_TOL
+    E, H2 = 4, 768
+    ws = [tuple(rng.standard_normal(s).astype(np.float32) / 8 for s in ((H2, M), (H2, M), (M, H2))) for _ in range(E)]
+    experts = [SlicedFFN(a, c, sp.SlicingRates(0.3, 0.2, 0.5), w3t=b, dtype="bf16", chunk_rows=128) for a, b, c in ws]
+    router = rng.standard_normal((M, E)).astype(np.float32).astype(np.float64)
+    xm = q(rng.standard_normal((T, M)))
+    got = np.asarray(SlicedMoE(experts, router, 2)(xm))
+    ref = orc.moe_forward(xm, [(q(a.T), q(b.T), q(c.T)) for a, b, c in ws], router, 2)
+    assert orc.max_rel_error(got, ref) <= BF16_TOL
