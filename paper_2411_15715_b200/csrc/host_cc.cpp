@@ -25,6 +25,8 @@ static const int g_cc_pf = env_or("SP_CC_PREFETCH", 8192);
 static const int g_amx = env_or("SP_AMX", 1);
 static const int g_amx_min_t = env_or("SP_AMX_MIN_T", 4);
 
+bool cc_uses_amx(const CCProblem& p) { return p.wdtype == 1 && g_amx && p.T >= g_amx_min_t && host_has_amx(); }
+
 // ---------------------------------------------------------------------------
 // thread pool: persistent workers, the caller participates as tid 0
 
@@ -323,7 +325,7 @@ void cc_forward_batch(const CCProblem* ps, int n, ThreadPool& pool, int threads)
       for (int64_t k = 0; k < p.T * p.N; ++k) p.y[k] = 0.f;
       continue;
     }
-    if (p.wdtype == 1 && g_amx && p.T >= g_amx_min_t && host_has_amx()) {
+    if (cc_uses_amx(p)) {
       cc_forward_amx(p, pool, threads);
       continue;
     }

@@ -60,6 +60,9 @@ struct CCProblem {
   int64_t ldx;
   int64_t T;
   float* y;        // [T, N] output
+  // AMX down phase: W2 of the CC rows already in VNNI pairs, one block per
+  // 128-column round (amx_prepack_w2), or null (each round repacks it)
+  const uint16_t* w2p = nullptr;
 };
 
 void cc_forward(const CCProblem& p, ThreadPool& pool, int threads);
@@ -75,5 +78,10 @@ bool host_has_avx512();
 // has AMX-BF16 (SP_AMX=0 disables it).
 bool host_has_amx();
 void cc_forward_amx(const CCProblem& p, ThreadPool& pool, int threads);
+// true when cc_forward / cc_forward_batch run this problem on AMX tiles
+bool cc_uses_amx(const CCProblem& p);
+// elements (bf16) of the prepacked W2 of p's CC rows, and the prepack itself
+size_t amx_w2_prepack_elems(const CCProblem& p);
+void amx_prepack_w2(const CCProblem& p, uint16_t* out, ThreadPool& pool, int threads);
 
 }  // namespace sp

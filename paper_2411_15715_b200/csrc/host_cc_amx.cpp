@@ -320,13 +320,49 @@ AMX_TARGET void up_worker(const AmxShared& S) {
     fprintf(stderr, "  up thread: %d slabs, kcycles tiles %llu act %llu\n", slabs, c_up >> 10, c_act >> 10);
 }
 
+// W2 rows of columns [n0, n0 + nr) in VNNI pairs: dst[kp][n][e] = W2[2 kp + e][n0 + n],
+// zero past b1 (b1p / 2 pairs)
+AMX_TARGET void repack_w2_round(const CCProblem& p, const int* chunk_of, int64_t b1p, int64_t n0, int64_t nr,
+                                uint16_t* w2p) {
+  const int64_t ldn = p.ldn;
+  for (int64_t kp = 0; kp < b1p / 2; ++kp) {
+    const int64_t ha = 2 * kp, hb = ha + 1;
+    uint16_t* dst = w2p + size_t(kp * nr * 2);
+    const uint16_t* ra = nullptr;
+    const uint16_t* rb = nullptr;
+    if (ha < p.b1) {
+      const HostChunk& c = p.chunks[chunk_of[size_t(ha)]];
+      ra = static_cast<const uint16_t*>(c.w2) + (ha - c.r0) * ldn + n0;
+    }
+    if (hb < p.b1) {
+      const HostChunk& c = p.chunks[chunk_of[size_t(hb)]];
+      rb = static_cast<const uint16_t*>(c.w2) + (hb - c.r0) * ldn + n0;
+    }
+    if (ha + 6 < p.b1) {  // the rows three pairs ahead
+      const HostChunk& c = p.chunks[chunk_of[size_t(ha + 6)]];
+      const char* q = reinterpret_cast<const char*>(static_cast<const uint16_t*>(c.w2) + (ha + 6 - c.r0) * ldn + n0);
+      for (int64_t off = 0; off < nr * 2; off += 64) _mm_prefetch(q + off, _MM_HINT_T0);
+      if (ha + 7 < p.b1)
+        for (int64_t off = 0; off < nr * 2; off += 64) _mm_prefetch(q + ldn * 2 + off, _MM_HINT_T0);
+    }
+    for (int64_t n = 0; n < nr; n += 16) {
+      const __m512i va = ra ? _mm512_cvtepu16_epi32(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(ra + n)))
+                            : _mm512_setzero_si512();
+      const __m512i vb = rb ? _mm512_slli_epi32(
+                                  _mm512_cvtepu16_epi32(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(rb + n))), 16)
+                            : _mm512_setzero_si512();
+      _mm512_storeu_si512(reinterpret_cast<void*>(dst + n * 2), _mm512_or_si512(va, vb));
+    }
+  }
+}
+
 // ---- phase 2: the down GEMM, kRoundCols output columns at a time ----
 AMX_TARGET void down_worker(const AmxShared& S, std::atomic<int64_t>* rounds, int tid) {
   const CCProblem& p = S.p;
   const int64_t T = p.T, N = p.N, T16 = S.T16, G16 = S.G16, n16 = S.n16, b1p = S.b1p, ldn = S.ldn;
   const int64_t ntiles = n16 / 16, per = kRoundCols / 16;
   static thread_local Scratch w2ps, ys;
-  uint16_t* const w2p = w2ps.get(size_t(b1p / 2 * kRoundCols * 2));
+  uint16_t* const w2p = p.w2p ? nullptr : w2ps.get(size_t(b1p / 2 * kRoundCols * 2));
   float* const ybuf = reinterpret_cast<float*>(ys.get(size_t(T16 * kRoundCols * 2)));  // [T16][nr] fp32
   tile_config();
   static const bool prof = getenv("SP_AMX_PROF") != nullptr;
@@ -337,36 +373,13 @@ AMX_TARGET void down_worker(const AmxShared& S, std::atomic<int64_t>* rounds, in
     if (prof) tc = __rdtsc();
     const int64_t je = std::min(ntiles, jr + per);
     const int64_t n0 = 16 * jr, nr = 16 * (je - jr);
-    // W2 rows of the round's columns in VNNI pairs: w2p[kp][n][e] = W2[2 kp + e][n0 + n], 0 past b1
-    for (int64_t kp = 0; kp < b1p / 2; ++kp) {
-      const int64_t ha = 2 * kp, hb = ha + 1;
-      uint16_t* dst = w2p + size_t(kp * nr * 2);
-      const uint16_t* ra = nullptr;
-      const uint16_t* rb = nullptr;
-      if (ha < p.b1) {
-        const HostChunk& c = p.chunks[S.chunk_of[size_t(ha)]];
-        ra = static_cast<const uint16_t*>(c.w2) + (ha - c.r0) * ldn + n0;
-      }
-      if (hb < p.b1) {
-        const HostChunk& c = p.chunks[S.chunk_of[size_t(hb)]];
-        rb = static_cast<const uint16_t*>(c.w2) + (hb - c.r0) * ldn + n0;
-      }
-      if (ha + 6 < p.b1) {  // the rows three pairs ahead
-        const HostChunk& c = p.chunks[S.chunk_of[size_t(ha + 6)]];
-        const char* q = reinterpret_cast<const char*>(static_cast<const uint16_t*>(c.w2) + (ha + 6 - c.r0) * ldn + n0);
-        for (int64_t off = 0; off < nr * 2; off += 64) _mm_prefetch(q + off, _MM_HINT_T0);
-        if (ha + 7 < p.b1)
-          for (int64_t off = 0; off < nr * 2; off += 64) _mm_prefetch(q + ldn * 2 + off, _MM_HINT_T0);
-      }
-      for (int64_t n = 0; n < nr; n += 16) {
-        const __m512i va = ra ? _mm512_cvtepu16_epi32(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(ra + n)))
-                              : _mm512_setzero_si512();
-        const __m512i vb = rb ? _mm512_slli_epi32(
-                                    _mm512_cvtepu16_epi32(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(rb + n))), 16)
-                              : _mm512_setzero_si512();
-        _mm512_storeu_si512(reinterpret_cast<void*>(dst + n * 2), _mm512_or_si512(va, vb));
-      }
-    }
+    // W2 rows of the round's columns in VNNI pairs: prepacked once per layer
+    // (amx_prepack_w2), else repacked here
+    const uint16_t* w2r = w2p;
+    if (p.w2p)
+      w2r = p.w2p + size_t(b1p) * size_t(n0);
+    else
+      repack_w2_round(p, S.chunk_of, b1p, n0, nr, w2p);
     if (prof) {
       c_rep += __rdtsc() - tc;
       tc = __rdtsc();
@@ -393,7 +406,7 @@ AMX_TARGET void down_worker(const AmxShared& S, std::atomic<int64_t>* rounds, in
             if (g2) TLOAD(2, y0 + 16 * nr, nr * 4);
             if (g2 && j2) TLOAD(3, y0 + 16 * nr + 16, nr * 4);
           }
-          const uint16_t* b0 = w2p + jn * 32;
+          const uint16_t* b0 = w2r + jn * 32;
           // software pipelined like the up loop: each tile of the next hidden
           // step is loaded right after its last reader in this one
           const int64_t s0 = kc / 32, se = ke / 32;
@@ -447,6 +460,28 @@ bool host_has_amx() {
   }();
   return ok;
 #endif
+}
+
+size_t amx_w2_prepack_elems(const CCProblem& p) {
+  const int64_t b1p = (p.b1 + 31) / 32 * 32, n16 = (p.N + 15) / 16 * 16;
+  return size_t(b1p) * size_t(n16);
+}
+
+// round r (columns [128 r, 128 r + nr_r)) at out + b1p * 128 r, laid out as the
+// down phase's repack: [b1p / 2][nr_r][2]
+void amx_prepack_w2(const CCProblem& p, uint16_t* out, ThreadPool& pool, int threads) {
+  const int64_t b1p = (p.b1 + 31) / 32 * 32, n16 = (p.N + 15) / 16 * 16;
+  std::vector<int> chunk_of(size_t(b1p), 0);
+  for (int c = 0; c < p.n_chunks; ++c)
+    for (int64_t r = 0; r < p.chunks[c].rc; ++r) chunk_of[size_t(p.chunks[c].r0 + r)] = c;
+  const int64_t n_rounds = (n16 + kRoundCols - 1) / kRoundCols;
+  std::atomic<int64_t> next{0};
+  pool.run(int(std::min<int64_t>(std::max(1, std::min(threads, pool.size())), n_rounds)), [&](int, int) {
+    for (int64_t r; (r = next.fetch_add(1)) < n_rounds;) {
+      const int64_t n0 = r * kRoundCols, nr = std::min(kRoundCols, n16 - n0);
+      repack_w2_round(p, chunk_of.data(), b1p, n0, nr, out + size_t(b1p) * size_t(n0));
+    }
+  });
 }
 
 void cc_forward_amx(const CCProblem& p, ThreadPool& pool, int threads) {

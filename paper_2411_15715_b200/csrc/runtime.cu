@@ -284,6 +284,9 @@ struct sp_layer {
   size_t host_map_bytes = 0;  // > 0: host region is an mmap'd (THP) range registered with CUDA
   int n_cc_chunks = 0;
   size_t max_chunk_bytes = 0;
+  // the CC rows' W2 in the AMX down phase's VNNI round blocks (sp::amx_prepack_w2),
+  // built at the layer's first AMX CC block (SP_CC_PREPACK=0: never)
+  uint16_t* w2_vnni = nullptr;
 };
 
 namespace sp {
@@ -665,6 +668,7 @@ static const int g_gg_last = env_int("SP_GG_LAST", 2);
 // SP_Y_ZERO_COPY=0: small host outputs go through a device buffer and a read-back copy
 static const bool g_y_zero_copy = env_int("SP_Y_ZERO_COPY", 1) != 0;
 static const bool g_host_merge = env_int("SP_HOST_MERGE", 1) != 0;
+static const bool g_cc_prepack = env_int("SP_CC_PREPACK", 1) != 0;
 constexpr size_t kZeroCopyY = size_t(256) << 10;
 constexpr int kTcMaxSplits = 24;
 // finalize: per-token rows kernel up to this many slices per call, slice groups beyond
@@ -1444,6 +1448,17 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         hcs.push_back(host_cc_chunks(L));
         probs.push_back(CCProblem{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, L->ldn, hcs.back().data(),
                                   L->n_cc_chunks, L->d.b1, xs, ldx, Tcc, reinterpret_cast<float*>(hp + p_ycc[c])});
+        if (g_cc_prepack && !cc_fn && cc_uses_amx(probs.back())) {
+          // once per layer: W2 of the CC rows repacked for the AMX down phase (forwards
+          // are serialised by the context lock, so no other CC job sees the layer now)
+          sp_layer* Lm = const_cast<sp_layer*>(L);
+          if (!Lm->w2_vnni) {
+            const size_t elems = amx_w2_prepack_elems(probs.back());
+            Lm->w2_vnni = static_cast<uint16_t*>(aligned_alloc(64, (elems * 2 + 63) / 64 * 64));
+            if (Lm->w2_vnni) amx_prepack_w2(probs.back(), Lm->w2_vnni, *C->pool, C->host_threads);
+          }
+          probs.back().w2p = Lm->w2_vnni;
+        }
         bytes += double(L->cc_bytes);
       }
       const int cc_threads = (flags & SP_NO_CC_THREADS) ? 1 : C->host_threads;
@@ -2140,6 +2155,8 @@ static void free_layer_memory(sp_layer* L) {
     L->host_only ? free(L->host) : (void)cudaFreeHost(L->host);
   }
   L->host = nullptr;
+  free(L->w2_vnni);
+  L->w2_vnni = nullptr;
 }
 
 // Validate, then place an empty layer (caller holds C->mu).
@@ -2381,12 +2398,26 @@ int sp_cc_forward_host(sp_layer_t L, const void* x, int xdtype, int64_t T, float
   CCProblem pr{L->d.wdtype, L->d.gated, L->d.act, M, N, L->ldm, L->ldn, hc.data(), L->n_cc_chunks,
                L->d.b1, xh.data(), ldx, T, y_cc};
   Context* C = ctx_or_null();
+  // the layer's prepacked W2 for the AMX down phase, as a forward's CC block uses
+  // it (only under C->mu, like every other use of it)
+  auto prepack = [&](ThreadPool& pool, int nthr) {
+    if (!g_cc_prepack || !cc_uses_amx(pr)) return;
+    if (!L->w2_vnni) {
+      const size_t elems = amx_w2_prepack_elems(pr);
+      L->w2_vnni = static_cast<uint16_t*>(aligned_alloc(64, (elems * 2 + 63) / 64 * 64));
+      if (L->w2_vnni) amx_prepack_w2(pr, L->w2_vnni, pool, nthr);
+    }
+    pr.w2p = L->w2_vnni;
+  };
   if (C && threads != 1) {
     // the pool is shared with forwards' CC blocks and ThreadPool::run is not
     // re-entrant: hold the context lock (a forward holds it until its CC join)
     std::lock_guard<std::mutex> g(C->mu);
-    cc_forward(pr, *C->pool, threads > 0 ? threads : C->host_threads);
+    const int nthr = threads > 0 ? threads : C->host_threads;
+    prepack(*C->pool, nthr);
+    cc_forward(pr, *C->pool, nthr);
   } else {
+    // unlocked: the layer's prepacked W2 (built and read under C->mu) is not touched
     ThreadPool local(std::max(1, threads));
     cc_forward(pr, local, std::max(1, threads));
   }

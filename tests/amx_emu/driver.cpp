@@ -1,5 +1,6 @@
 // Test driver for the AMX CC kernel built with SP_AMX_EMULATE (software tiles):
-// lays bf16 weights out as the runtime's CC chunks and runs cc_forward_amx.
+// lays bf16 weights out as the runtime's CC chunks and runs cc_forward_amx
+// (with prepack: on the prepacked W2 copy, as the runtime does after a layer's first AMX call).
 #include <stdint.h>
 #include <string.h>
 
@@ -9,7 +10,7 @@
 
 extern "C" int amx_emu_run(int gated, int act, int64_t M, int64_t N, int64_t b1, int64_t chunk_rows,
                            const uint16_t* w1t, const uint16_t* w3t, const uint16_t* w2,  // [b1, M] / [b1, M] / [b1, N]
-                           const float* x, int64_t T, float* y, int threads) {
+                           const float* x, int64_t T, float* y, int threads, int prepack) {
   const int64_t ldm = (M + 63) / 64 * 64, ldn = (N + 63) / 64 * 64, ldx = ldm;
   std::vector<std::vector<uint16_t>> store;
   std::vector<sp::HostChunk> chunks;
@@ -29,6 +30,12 @@ extern "C" int amx_emu_run(int gated, int act, int64_t M, int64_t N, int64_t b1,
   for (int64_t t = 0; t < T; ++t) memcpy(&xs[size_t(t * ldx)], x + t * M, size_t(M) * 4);
   sp::CCProblem p{1, gated, act, M, N, ldm, ldn, chunks.data(), int(chunks.size()), b1, xs.data(), ldx, T, y};
   sp::ThreadPool pool(threads);
+  std::vector<uint16_t> w2p;
+  if (prepack) {  // the layer-level VNNI copy of W2 the runtime builds once (amx_prepack_w2)
+    w2p.assign(sp::amx_w2_prepack_elems(p), 0xffff);
+    sp::amx_prepack_w2(p, w2p.data(), pool, threads);
+    p.w2p = w2p.data();
+  }
   sp::cc_forward_amx(p, pool, threads);
   return 0;
 }

@@ -38,7 +38,7 @@ def emu(tmp_path_factory):
     lib = C.CDLL(str(out))
     lib.amx_emu_run.restype = C.c_int
     lib.amx_emu_run.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
-                                C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int]
+                                C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int, C.c_int]
     return lib
 
 
@@ -65,7 +65,8 @@ def _reference(x, w1t, w3t, w2, act, gated):
     (128, 512, 544, 500, 192, 1, "silu", 8),  # a down round of 128 columns and a partial one
     (20, 1100, 96, 1100, 256, 1, "silu", 3),  # K and the hidden range over several 1024-wide chunks
 ])
-def test_amx_kernel_emulated_matches_restatement(emu, T, M, N, b1, chunk, gated, act, threads):
+@pytest.mark.parametrize("prepack", [0, 1])
+def test_amx_kernel_emulated_matches_restatement(emu, T, M, N, b1, chunk, gated, act, threads, prepack):
     rng = np.random.default_rng(T * 7 + M)
     x = rng.uniform(-1, 1, (T, M)).astype(np.float32)
     w1t = (rng.standard_normal((b1, M)) / np.sqrt(M)).astype(np.float32)
@@ -75,7 +76,7 @@ def test_amx_kernel_emulated_matches_restatement(emu, T, M, N, b1, chunk, gated,
     acts = {"identity": 0, "silu": 1, "gelu": 2}
     b_w1, b_w3, b_w2 = (np.ascontiguousarray(_bits(a)) for a in (w1t, w3t, w2))
     st = emu.amx_emu_run(gated, acts[act], M, N, b1, chunk, b_w1.ctypes.data, b_w3.ctypes.data, b_w2.ctypes.data,
-                         x.ctypes.data, T, y.ctypes.data, threads)
+                         x.ctypes.data, T, y.ctypes.data, threads, prepack)
     assert st == 0 and np.isfinite(y).all()
     ref = _reference(x, w1t, w3t, w2, act, gated)
     assert orc.max_rel_error(y, ref) <= 2e-3, orc.max_rel_error(y, ref)
@@ -83,15 +84,17 @@ def test_amx_kernel_emulated_matches_restatement(emu, T, M, N, b1, chunk, gated,
 
 def test_amx_kernel_emulated_is_thread_count_invariant(emu):
     """Columns are split over threads, each output summed in one hidden order:
-    bit-identical for any thread count."""
+    bit-identical for any thread count, with or without the prepacked W2."""
     rng = np.random.default_rng(11)
     T, M, N, b1 = 33, 160, 200, 150
     x = rng.uniform(-1, 1, (T, M)).astype(np.float32)
     ws = [np.ascontiguousarray(_bits((rng.standard_normal(s) / 8).astype(np.float32))) for s in ((b1, M), (b1, M), (b1, N))]
     outs = []
     for th in (1, 3, 7):
-        y = np.zeros((T, N), dtype=np.float32)
-        emu.amx_emu_run(1, 1, M, N, b1, 64, ws[0].ctypes.data, ws[1].ctypes.data, ws[2].ctypes.data, x.ctypes.data, T,
-                        y.ctypes.data, th)
-        outs.append(y)
+        for pre in (0, 1):
+            y = np.zeros((T, N), dtype=np.float32)
+            emu.amx_emu_run(1, 1, M, N, b1, 64, ws[0].ctypes.data, ws[1].ctypes.data, ws[2].ctypes.data,
+                            x.ctypes.data, T, y.ctypes.data, th, pre)
+            outs.append(y)
+    # and the prepacked W2 copy feeds the same tiles as the per-round repack
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
