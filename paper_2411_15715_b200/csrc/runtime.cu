@@ -1839,7 +1839,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     // a prompt's output is MBs, usually into a fresh (not yet faulted-in) array:
     // copy it out on the pool, in 64 KB-aligned shares
     const size_t ybytes = size_t(T) * N * yel;
-    const int nt = ybytes >= (size_t(1) << 20) ? C->pool->size() : 1;
+    const int nt = ybytes >= (size_t(256) << 10) ? C->pool->size() : 1;
     if (host_merge) {
       // y[t] = device part[t] + sum over t's entries (call c, row i, gate) with a CC
       // row of gate * y_cc_c[i], entries in the host CSR's order
@@ -1932,25 +1932,36 @@ __attribute__((optimize("fp-contract=off"))) static void route_logits(const floa
   }
 }
 
+// Tokens are independent (each logit is one serial m-ascending sum, ~8 us at
+// M = 4096), so a batch is routed on the host pool when one is given (the caller
+// holds the context lock): 32 tokens took ~0.3 ms on one thread, ahead of the
+// CC block and the first copy.
 static int moe_route(const float* router, int64_t M, int E, int k, const void* x, int xdtype, int64_t T,
-                     int32_t* ids, float* gates) {
+                     int32_t* ids, float* gates, ThreadPool* pool = nullptr, int threads = 1) {
   if (E < 1 || k < 1 || k > E) return fail(SP_ERR_VALUE, "top_k must lie in [1, %d], got %d", E, k);
-  std::vector<double> logit(static_cast<size_t>(E), 0.0);
-  std::vector<int> order(static_cast<size_t>(E), 0);
   const size_t xel = xdtype == SP_BF16 ? 2 : 4;
-  for (int64_t t = 0; t < T; ++t) {
-    route_logits(router, M, E, static_cast<const char*>(x) + size_t(t) * M * xel, xdtype, logit.data());
-    for (int e = 0; e < E; ++e) order[e] = e;
-    // k largest, ties to the lower expert id (a stable descending sort)
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return logit[a] > logit[b]; });
-    const double top = logit[order[0]];
-    double z = 0.0;
-    for (int j = 0; j < k; ++j) z += std::exp(logit[order[j]] - top);
-    for (int j = 0; j < k; ++j) {
-      ids[t * k + j] = order[j];
-      gates[t * k + j] = float(std::exp(logit[order[j]] - top) / z);
+  auto route_range = [&](int64_t t0, int64_t t1) {
+    std::vector<double> logit(static_cast<size_t>(E), 0.0);
+    std::vector<int> order(static_cast<size_t>(E), 0);
+    for (int64_t t = t0; t < t1; ++t) {
+      route_logits(router, M, E, static_cast<const char*>(x) + size_t(t) * M * xel, xdtype, logit.data());
+      for (int e = 0; e < E; ++e) order[e] = e;
+      // k largest, ties to the lower expert id (a stable descending sort)
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return logit[a] > logit[b]; });
+      const double top = logit[order[0]];
+      double z = 0.0;
+      for (int j = 0; j < k; ++j) z += std::exp(logit[order[j]] - top);
+      for (int j = 0; j < k; ++j) {
+        ids[t * k + j] = order[j];
+        gates[t * k + j] = float(std::exp(logit[order[j]] - top) / z);
+      }
     }
-  }
+  };
+  const int nt = pool && T >= 4 ? int(std::min<int64_t>(std::min(threads, pool->size()), T)) : 1;
+  if (nt > 1)
+    pool->run(nt, [&](int tid, int n) { route_range(T * tid / n, T * (tid + 1) / n); });
+  else
+    route_range(0, T);
   return SP_OK;
 }
 
@@ -1990,7 +2001,7 @@ static int moe_forward(Context* C, const sp_layer_t* layers, int E, const float*
   const double t_route1 = now_s();
   std::vector<int32_t> ids(static_cast<size_t>(T * k));
   std::vector<float> gates(static_cast<size_t>(T * k));
-  SP_TRY(moe_route(router, M, E, k, xh, xdtype, T, ids.data(), gates.data()));
+  SP_TRY(moe_route(router, M, E, k, xh, xdtype, T, ids.data(), gates.data(), C->pool.get(), C->host_threads));
   // group token rows by expert (ascending token order per expert)
   std::vector<std::vector<int32_t>> rows(static_cast<size_t>(E));
   std::vector<std::vector<float>> g(static_cast<size_t>(E));
