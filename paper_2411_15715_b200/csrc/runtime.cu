@@ -1499,7 +1499,12 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       round_bf16_host(static_cast<const float*>(x_src), reinterpret_cast<uint16_t*>(hp + p_x), T * M);
     else
       memcpy(hp + p_x, x, size_t(T) * M * xel);
-    SP_CUDA(cudaMemcpyAsync(dws + o_xdev, hp + p_x, size_t(T) * M * xel, cudaMemcpyHostToDevice, C->s_comp));
+    // on the copy stream, in line with the chunk copies (an H2D issued on the
+    // compute stream was observed to land only behind the ring's copies)
+    SP_CUDA(cudaStreamWaitEvent(C->s_copy, C->ev_ws, 0));
+    SP_CUDA(cudaMemcpyAsync(dws + o_xdev, hp + p_x, size_t(T) * M * xel, cudaMemcpyHostToDevice, C->s_copy));
+    SP_CUDA(cudaEventRecord(C->ev_x, C->s_copy));
+    SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_x, 0));
     x_dev = dws + o_xdev;
     return SP_OK;
   };
@@ -1593,9 +1598,16 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   // copies (behind them it waited for all of them: ~0.9 ms for a prompt's CC block)
   if (!cc_started) SP_TRY(start_cc());
 
-  // the first ring slots' copies go right behind the (tiny) metadata copies
+  // the first ring slots' copies go right behind the (tiny) metadata copies.
+  // A small host x is staged and copied first: its H2D queued behind the ring's
+  // copies would hold every GG block and chunk kernel for their whole duration
+  // (~0.9 ms); a prompt's x (MBs, ~1 ms of staging) goes behind them instead.
+  static const bool launch_prof = env_int("SP_LAUNCH_PROF", 0) != 0;
+  double lp[6] = {now_s(), 0, 0, 0, 0, 0};
+  if (size_t(T) * M * 2 <= (size_t(1) << 20)) SP_TRY(stage_x_dev());
   while (next_copy < items.size() && next_copy < size_t(ring_slots)) SP_TRY(enqueue_copy());
   SP_TRY(stage_x_dev());
+  lp[1] = now_s();
 
   // ---- GG blocks (HBM resident): the decode-size calls share one grouped launch ----
   // GG work is off the critical path (the copy stream paces the step), but it
@@ -1688,7 +1700,9 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   // (SP_GG_LAST, see g_gg_last)
   std::function<int()> gg_group_last;
   if (g_gg_last && has_group && !items.empty()) gg_group_last = std::move(gg_jobs[next_gg++]);
+  lp[2] = now_s();
   if (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());
+  lp[3] = now_s();
   if (items.empty())
     while (next_gg < gg_jobs.size()) SP_TRY(gg_jobs[next_gg++]());
 
@@ -1717,6 +1731,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       span.end();
     }
     SP_CUDA(cudaEventRecord(C->ev_free[it.slot], C->s_comp));
+    if (i == 0) lp[4] = now_s();
     if (next_copy < items.size()) SP_TRY(enqueue_copy());
     if (gg_group_last && g_gg_last == 1 && next_copy == items.size()) {
       SP_TRY(gg_group_last());  // every copy queued: the group hides under the ones in flight
@@ -1728,6 +1743,11 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   if (gg_group_last) SP_TRY(gg_group_last());
 
   const double t_enq_done = now_s();
+  if (launch_prof)
+    fprintf(stderr, "[launch] T %lld calls %d items %zu gg_jobs %zu | metadata+cc %.0f  ring copies %.0f  gg build %.0f  "
+            "first gg job %.0f  first chunk %.0f  rest %.0f us\n", (long long)T, n_calls, items.size(), gg_jobs.size(),
+            (lp[0] - t_call) * 1e6, (lp[1] - lp[0]) * 1e6, (lp[2] - lp[1]) * 1e6, (lp[3] - lp[2]) * 1e6,
+            (lp[4] > 0 ? lp[4] - lp[3] : 0) * 1e6, (t_enq_done - (lp[4] > 0 ? lp[4] : lp[3])) * 1e6);
   host_span(C, 0, SP_TRACE_LAUNCH, t_call, t_enq_done, 0.0);
 
   // ---- finalize: reduce slices + CC partials + gates + cast ----
