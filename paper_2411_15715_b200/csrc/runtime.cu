@@ -176,6 +176,7 @@ struct Context {
   int num_sms = 0;
   cudaStream_t s_comp = nullptr, s_copy = nullptr, s_aux = nullptr;
   cudaEvent_t ev_user, ev_x, ev_ycc, ev_done;
+  cudaEvent_t ev_meta = nullptr;  // on s_copy after a forward's metadata copies
   cudaEvent_t ev_copied[kMaxRingSlots], ev_free[kMaxRingSlots];
   DevBuf ring[kMaxRingSlots];
   size_t ring_bytes = 0;
@@ -195,6 +196,10 @@ struct Context {
   DevBuf tc_partial;  // split-K partial tiles of the tensor-core GEMMs
   DevBuf tc_tickets;  // per-tile split tickets (zero, re-armed by the last split)
   DevBuf tc_z;        // up-GEMM split partials of the pre-activations
+  // a forward's device metadata (token ids, gates, finalize CSR), alternating
+  // like the pinned halves: half hb's previous user finished (hpin_done[hb]),
+  // so it is overwritten from the copy stream without waiting on s_comp
+  DevBuf dmeta[2];
   std::vector<float> hscratch;
   std::unique_ptr<ThreadPool> pool;
   int host_threads = 1;
@@ -1273,7 +1278,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     dev_off += size_t(round_up(int64_t(bytes), 256));
     return o;
   };
-  std::vector<size_t> o_part(n_calls), o_ycc(n_calls), o_ids(n_calls), o_g(n_calls), o_xtc(n_calls),
+  std::vector<size_t> o_part(n_calls), o_ycc(n_calls), o_xtc(n_calls),
       o_atc(n_calls);
   std::vector<int64_t> ws_ld_a(n_calls);
   std::vector<int> ws_split(n_calls, 0);
@@ -1301,11 +1306,12 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     o_xtc[c] = tc ? dalloc(size_t(Te) * L->ldm * 2) : SIZE_MAX;
     o_atc[c] = tc ? dalloc(size_t(Te) * ws_ld_a[c] * 2) : SIZE_MAX;
     o_ycc[c] = dalloc(size_t(Te) * N * 4);
-    o_ids[c] = dalloc(size_t(Te) * 4);
-    o_g[c] = dalloc(size_t(Te) * 4);
     total_rows += Te;
   }
-  const size_t o_csr = dalloc(size_t(T + 1 + 3 * total_rows) * 4);
+  // device metadata (dmeta[hb]): per call [token ids | gates] as the pinned
+  // block, then the finalize CSR -- two copies
+  const size_t meta_bytes = size_t(round_up(int64_t(total_rows) * 8, 256));
+  const size_t csr_bytes = size_t(T + 1 + 3 * total_rows) * 4;
   const size_t o_xdev = dalloc(host_io ? size_t(T) * M * xel : 0);
   const size_t o_ydev = dalloc(host_io ? size_t(T) * N * yel : 0);
   SP_TRY(C->ws.ensure(dev_off, C->s_comp));
@@ -1313,6 +1319,12 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   // this point: the (stream-ordered) allocation and the previous forward's finalize
   SP_CUDA(cudaEventRecord(C->ev_ws, C->s_comp));
   char* dws = static_cast<char*>(C->ws.p);
+  const int hb = C->hpin_turn;
+  C->hpin_turn ^= 1;
+  if (C->hpin_used[hb]) SP_CUDA(cudaEventSynchronize(C->hpin_done[hb]));
+  SP_TRY(C->dmeta[hb].ensure(meta_bytes + csr_bytes));
+  char* const dmeta = static_cast<char*>(C->dmeta[hb].p);
+  int64_t meta_off = 0;
   for (int c = 0; c < n_calls; ++c) {
     ws[c].part = reinterpret_cast<float*>(dws + o_part[c]);
     ws[c].S = 0;
@@ -1323,8 +1335,9 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
       ws[c].a_tc = reinterpret_cast<__nv_bfloat16*>(dws + o_atc[c]);
     }
     ws[c].ycc = reinterpret_cast<float*>(dws + o_ycc[c]);
-    ws[c].ids = reinterpret_cast<int32_t*>(dws + o_ids[c]);
-    ws[c].gates = reinterpret_cast<float*>(dws + o_g[c]);
+    ws[c].ids = reinterpret_cast<int32_t*>(dmeta + size_t(meta_off) * 8);
+    ws[c].gates = reinterpret_cast<float*>(dmeta + size_t(meta_off) * 8 + size_t(calls[c].tokens) * 4);
+    meta_off += calls[c].tokens;
   }
 
   // pinned staging: [meta (ids+gates) | x | ycc per call | y]
@@ -1343,9 +1356,6 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   // Small host outputs are written by the finalize kernel straight into pinned
   // host memory (mapped, unified addressing): no read-back copy after it.
   const bool y_zero_copy = host_io && g_y_zero_copy && size_t(T) * N * yel <= kZeroCopyY;
-  const int hb = C->hpin_turn;
-  C->hpin_turn ^= 1;
-  if (C->hpin_used[hb]) SP_CUDA(cudaEventSynchronize(C->hpin_done[hb]));
   SP_TRY(C->hpin[hb].ensure(pin_off));
   char* hp = static_cast<char*>(C->hpin[hb].p);
   // Any error return from here on leaves no work behind: the CC job (which
@@ -1562,10 +1572,6 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         ids[i] = calls[c].token_ids ? calls[c].token_ids[i] : int32_t(i);
         g[i] = calls[c].gates ? calls[c].gates[i] : 1.0f;
       }
-      if (Te > 0) {
-        SP_CUDA(cudaMemcpyAsync(ws[c].ids, ids, Te * 4, cudaMemcpyHostToDevice, C->s_comp));
-        SP_CUDA(cudaMemcpyAsync(ws[c].gates, g, Te * 4, cudaMemcpyHostToDevice, C->s_comp));
-      }
       mo += Te * 8;
     }
   }
@@ -1590,8 +1596,14 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
         crow[slot] = int32_t(i);
         cgate[slot] = calls[c].gates ? calls[c].gates[i] : 1.0f;
       }
-    SP_CUDA(cudaMemcpyAsync(dws + o_csr, cs, size_t(T + 1 + 3 * total_rows) * 4, cudaMemcpyHostToDevice,
-                            C->s_comp));
+    // both metadata blocks on the copy stream, ahead of the chunk copies: small
+    // H2D copies on the compute stream were observed to land only behind the
+    // ring's copies, holding the step's first kernels (~0.9 ms at 6 slots)
+    if (total_rows > 0)
+      SP_CUDA(cudaMemcpyAsync(dmeta, hp + p_meta, size_t(total_rows) * 8, cudaMemcpyHostToDevice, C->s_copy));
+    SP_CUDA(cudaMemcpyAsync(dmeta + meta_bytes, cs, csr_bytes, cudaMemcpyHostToDevice, C->s_copy));
+    SP_CUDA(cudaEventRecord(C->ev_meta, C->s_copy));
+    SP_CUDA(cudaStreamWaitEvent(C->s_comp, C->ev_meta, 0));
   }
 
   // x only on the device: its read-back for the CC block goes ahead of the ring
@@ -1761,7 +1773,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
   fa.out = y_zero_copy ? static_cast<void*>(hp + p_y) : host_io ? static_cast<void*>(dws + o_ydev) : y;
   fa.odtype = ydtype;
   {
-    const int32_t* cs = reinterpret_cast<const int32_t*>(dws + o_csr);
+    const int32_t* cs = reinterpret_cast<const int32_t*>(dmeta + meta_bytes);
     fa.entry_start = cs;
     fa.entry_call = cs + (T + 1);
     fa.entry_row = fa.entry_call + total_rows;
@@ -2106,7 +2118,7 @@ int sp_init(int device, int host_threads) {
   SP_CUDA(cudaStreamCreateWithFlags(&C->s_comp, cudaStreamNonBlocking));
   SP_CUDA(cudaStreamCreateWithFlags(&C->s_copy, cudaStreamNonBlocking));
   SP_CUDA(cudaStreamCreateWithFlags(&C->s_aux, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&C->ev_user, &C->ev_x, &C->ev_ycc, &C->ev_done, &C->ev_ws, &C->hpin_done[0],
+  for (cudaEvent_t* e : {&C->ev_user, &C->ev_x, &C->ev_ycc, &C->ev_done, &C->ev_ws, &C->ev_meta, &C->hpin_done[0],
                          &C->hpin_done[1]})
     SP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   for (int i = 0; i < kMaxRingSlots; ++i) {
@@ -2141,7 +2153,7 @@ int sp_shutdown(void) {
   }
   if (C->cc_thread.joinable()) C->cc_thread.join();
   cudaDeviceSynchronize();
-  for (cudaEvent_t e : {C->ev_user, C->ev_x, C->ev_ycc, C->ev_done, C->ev_ws, C->hpin_done[0], C->hpin_done[1]})
+  for (cudaEvent_t e : {C->ev_user, C->ev_x, C->ev_ycc, C->ev_done, C->ev_ws, C->ev_meta, C->hpin_done[0], C->hpin_done[1]})
     cudaEventDestroy(e);
   for (int i = 0; i < kMaxRingSlots; ++i) {
     cudaEventDestroy(C->ev_copied[i]);
