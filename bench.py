@@ -90,6 +90,9 @@ def parse(argv=None):
     ap.add_argument("--calibrate", type=int, default=1,
                     help="rescale the profile's host CPU / link terms from traced steps on this box and re-solve")
     ap.add_argument("--calib-steps", type=int, default=16)
+    ap.add_argument("--calib-rounds", type=int, default=1,
+                    help="calibrate -> re-solve -> re-slice rounds; stops early once r_CC moves < --calib-tol")
+    ap.add_argument("--calib-tol", type=float, default=0.005)
     args = ap.parse_args(argv)
     if args.config == "cfg1":
         args.model_dim, args.hidden_dim, args.dtype = 1024, 3584, "f32"
@@ -117,8 +120,9 @@ def metric_name(args):
         name = "PhiMoE 16x(4096/6400)" if args.moe == "phimoe" else "Mixtral-8x22B 8x(6144/16384)"
         return f"decode tokens/s, {name} MoE FFN layer top-2, expert-parallel, batch {args.batch}/GPU"
     if args.config == "cfg3":
-        return ("prefill tokens/s, Mixtral-8x7B 32-layer MoE FFN stack, 512-token prompt with the "
-                "token-assignment split (n_g from solve_ng), then 128 decode steps")
+        plan = "n_g from solve_ng" if args.token_plan == "solve_ng" else "per-layer token plan"
+        return (f"prefill tokens/s, Mixtral-8x7B {args.layers}-layer MoE FFN stack, {args.prompt}-token prompt "
+                f"with the token-assignment split ({plan}), then {args.decode_steps} decode steps")
     if args.config == "cfg1":
         return "decode tokens/s, MoE FFN layer 1024/3584 (8 experts top-2) fp32, fixed CC/CG/GG 0.2/0.3/0.5"
     return "decode tokens/s, Mixtral-8x7B MoE FFN layer (4096/14336, 8 experts top-2), sliced CC/CG/GG"
@@ -219,7 +223,12 @@ def plan_rates(args, tokens_per_step):
     else:
         n_gemms, t_expert = 3, max(1, tokens_per_step)
     profile, source = load_profile(decode_profile_for(args.profile, t_expert))
-    layer = sp.LayerSpec(args.model_dim, hidden, n_gemms=n_gemms, precision=sp.Precision.FP16)
+    # The reference's Precision has 2-byte and 4-bit weights only (perf_model.py:45-51).
+    # fp32 weights (cfg1) are modelled as a twice-as-wide 2-byte layer: every term of
+    # the decode model is bytes-bound (weight stream, CC rows, CG copies), so twice
+    # the bytes per GEMM is twice the units at the same per-unit rates.
+    layer = sp.LayerSpec(args.model_dim, hidden * (2 if args.dtype == "f32" else 1), n_gemms=n_gemms,
+                         precision=sp.Precision.FP16)
     wl = sp.Workload(tokens=t_expert, phase=sp.Phase.GENERATION)
     args.plan_layer, args.plan_workload = layer, wl  # what predict_step() evaluates
     budget = args.budget_frac * layer.layer_bytes
@@ -673,35 +682,52 @@ def run_ours(args):
     # ---- per-box recalibration of the host terms, then re-plan (before timing) ----
     calib = None
     if args.calibrate and args.config != "cfg1" and (args.experts > 1 or args.config == "cfg4"):
-        t_cal = time.perf_counter()
-        rates0, profile0 = rates, profile
-        _, _, _, cspans = timed(args.calib_steps, trace="full")
-        profile, calib = calibrate_host_terms(args, profile, rates, cspans, args.calib_steps)
-        rates = solve_rates(args, profile, budget)
-        source += f" (host terms recalibrated on this box: CPU x{calib['k_cpu']:.3f}, link x{calib['k_link']:.3f})"
+        # Fixed-point rounds: trace the step at the current split, rescale the
+        # host terms by measured / predicted, re-solve, re-slice, repeat until
+        # the split stops moving.  One round re-anchors the model at the OLD
+        # split only; where the host's per-row CC cost depends on the split
+        # itself (batched decode: CC block on the critical path or not, shared
+        # host DRAM with the copies), the next round measures the new split.
         from dataclasses import asdict
 
         from paper_2411_15715_b200.sliced import split_boundaries
 
+        t_cal = time.perf_counter()
+        rates0, profile0 = rates, profile
         t_fin0 = predict_step(args, rates0, profile0)["t_fin_s"]
-        resliced = False
-        w0 = next(iter(experts.values())).block_widths if experts else None
-        if experts and tuple(split_boundaries(w0[0] + w0[1] + w0[2], rates)) != (w0[0], w0[0] + w0[1]):
-            new_experts = {e: ex.reslice(rates) for e, ex in experts.items()}
-            for ex in experts.values():
-                ex.layer.release()
-            experts = new_experts
-            resliced = True
-            if args.config == "cfg4":
-                moe = ColumnShardedFFN(experts[rank])
-            else:
-                moe = ExpertParallelMoE(experts, router, args.top_k, args.experts, out_dim=args.model_dim)
-            for i in range(args.warmup):
-                step(i)
-                step(i, host_io=True)
-            torch.cuda.synchronize()
-        calib.update({"rates_before": asdict(rates0), "rates_after": asdict(rates), "resliced": resliced,
-                      "t_fin_pred_before_s": t_fin0, "seconds": time.perf_counter() - t_cal})
+        rounds, k_cpu_tot, k_link_tot, resliced = [], 1.0, 1.0, False
+        for _ in range(max(1, args.calib_rounds)):
+            _, _, _, cspans = timed(args.calib_steps, trace="full")
+            profile, info = calibrate_host_terms(args, profile, rates, cspans, args.calib_steps)
+            k_cpu_tot *= info["k_cpu"]
+            k_link_tot *= info["k_link"]
+            new_rates = solve_rates(args, profile, budget)
+            info.update(rates=asdict(rates), rates_next=asdict(new_rates))
+            rounds.append(info)
+            moved = abs(new_rates.cc - rates.cc) > args.calib_tol or abs(new_rates.cg - rates.cg) > args.calib_tol
+            w0 = next(iter(experts.values())).block_widths if experts else None
+            if experts and tuple(split_boundaries(w0[0] + w0[1] + w0[2], new_rates)) != (w0[0], w0[0] + w0[1]):
+                new_experts = {e: ex.reslice(new_rates) for e, ex in experts.items()}
+                for ex in experts.values():
+                    ex.layer.release()
+                experts = new_experts
+                resliced = True
+                if args.config == "cfg4":
+                    moe = ColumnShardedFFN(experts[rank])
+                else:
+                    moe = ExpertParallelMoE(experts, router, args.top_k, args.experts, out_dim=args.model_dim)
+                for i in range(args.warmup):
+                    step(i)
+                    step(i, host_io=True)
+                torch.cuda.synchronize()
+            rates = new_rates
+            if not moved:
+                break
+        source += f" (host terms recalibrated on this box: CPU x{k_cpu_tot:.3f}, link x{k_link_tot:.3f})"
+        calib = {"k_cpu": k_cpu_tot, "k_link": k_link_tot, "steps": args.calib_steps,
+                 "cpu_busy_s": rounds[-1]["cpu_busy_s"], "transfer_busy_s": rounds[-1]["transfer_busy_s"],
+                 "rounds": rounds, "rates_before": asdict(rates0), "rates_after": asdict(rates),
+                 "resliced": resliced, "t_fin_pred_before_s": t_fin0, "seconds": time.perf_counter() - t_cal}
 
     clk = ClockSampler(local).start()
     clk.armed = True
@@ -996,7 +1022,8 @@ def run_prefill_decode(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_p * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (random-init weights, seeded)",
         "decode_tokens_per_s": args.decode_steps / t_d, "decode_ms_per_token": t_d / args.decode_steps * 1e3,
-        "config": {"workload": "mixtral-8x7b-32layer-prefill512-decode128", "layers": args.layers,
+        "config": {"workload": f"mixtral-8x7b-{args.layers}layer-prefill{args.prompt}-decode{args.decode_steps}",
+                   "layers": args.layers,
                    "distinct_weight_sets": D, "prompt_tokens": args.prompt, "decode_steps": args.decode_steps,
                    "model_dim": args.model_dim, "hidden_dim": args.hidden_dim, "experts": args.experts,
                    "top_k": args.top_k, "rates": {"cc": rates.cc, "cg": rates.cg, "gg": rates.gg},
