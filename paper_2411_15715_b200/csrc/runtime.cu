@@ -812,11 +812,16 @@ static int launch_gemm_pair(Context* C, int nt, const CUtensorMap& a0, const CUt
                             const tc::GemmArgs& g, cudaStream_t s, bool pdl) {
   switch (nt) {
     case 256: return launch_gemm_pair_t<256, NA>(C, a0, a1, b, g, s, pdl);
+    case 128: return launch_gemm_pair_t<128, NA>(C, a0, a1, b, g, s, pdl);
+    case 64: return launch_gemm_pair_t<64, NA>(C, a0, a1, b, g, s, pdl);
+    case 32: return launch_gemm_pair_t<32, NA>(C, a0, a1, b, g, s, pdl);
     default: return fail(SP_ERR_VALUE, "CTA-pair up GEMM: no %d-token tile", nt);
   }
 }
 // SP_TC_PAIR=0 keeps every up GEMM on single-CTA tiles
 static const bool g_tc_pair = env_int("SP_TC_PAIR", 1) != 0;
+// smallest token tile that runs the up GEMM on CTA pairs (SP_TC_PAIR_MIN_NT)
+static const int g_tc_pair_min_nt = env_int("SP_TC_PAIR_MIN_NT", 256);
 
 // Split K so the launch puts ~`target` CTAs to work (bounded by the k-blocks).
 static int split_k(int tiles, int k, int target) {
@@ -840,7 +845,11 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
   const int nt = T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256;
   const int t_tiles = int((T + nt - 1) / nt);
   // HBM-resident blocks spread over every SM; streamed chunks hide under their copy
+  // (SP_TC_UP_CTAS / SP_TC_DN_CTAS: probe overrides of the resident targets)
+  static const int up_ctas_env = env_int("SP_TC_UP_CTAS", 0), dn_ctas_env = env_int("SP_TC_DN_CTAS", 0);
   const int target = resident ? C->num_sms : 32;
+  const int up_target = resident && up_ctas_env > 0 ? up_ctas_env : target;
+  const int dn_target = resident && dn_ctas_env > 0 ? dn_ctas_env : target;
   const int na = L->d.gated ? 2 : 1;
   tc::GemmArgs up{};
   up.mode = L->d.gated ? tc::kUpGated : tc::kUpPlain;
@@ -850,7 +859,7 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
   up.k = int(M);
   up.m_tiles = int((R + tc::BM - 1) / tc::BM);
   up.t_tiles = t_tiles;
-  up.ks = split_k(up.m_tiles * t_tiles, int(M), target);
+  up.ks = split_k(up.m_tiles * t_tiles, int(M), up_target);
   up.a_out = w.a_tc;
   up.lda = w.ld_a;
   if (up.ks > 1) {
@@ -871,7 +880,7 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
   dn.ldy = N;
   if (resident) {
     // HBM-resident block: split K over ~every SM, one output slice per split
-    dn.ks = std::min(split_k(dn.m_tiles * t_tiles, int(R), target), w.split_capacity);
+    dn.ks = std::min(split_k(dn.m_tiles * t_tiles, int(R), dn_target), w.split_capacity);
     dn.split_slices = 1;
     dn.y_split_stride = int64_t(T_e) * N;
     if (t0 > 0 || T < T_e)  // rows outside [t0, t0 + T) of the new slices must read as zero
@@ -900,7 +909,7 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
     SP_CUDA(cudaGetLastError());
     ++C->launches;
   }
-  if (g_tc_pair && nt == 256) {
+  if (g_tc_pair && nt >= std::max(32, g_tc_pair_min_nt)) {
     // x tile split across the two SMs of a CTA pair: 25 % fewer bytes into each SM.
     // Measured (ncu, 14336-row expert): T = 512 up GEMM 153 -> 141 us, T = 256
     // expert 134 -> 129 us; at 64/128-token tiles it was within +-4 % either way.
