@@ -354,11 +354,18 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
     mbar_wait(&full[slot], (s / NST) & 1);
     const int rows_s = min(fp.rs_up, n_local - s * fp.rs_up);
     const unsigned char* st = ring + size_t(slot) * fp.stage_bytes;
-    // the stage's rows together: RSU x G x TT independent accumulators
+    // the stage's rows together: RSU x G x TT independent accumulators, updated
+    // in pairs (W1 / W3 of a row, or two rows) by packed FFMA2 with x broadcast:
+    // each lane of an FFMA2 is the same fma.rn as a scalar FFMA, so every
+    // accumulator sees the identical sequence -- half the FMA instructions
+    constexpr int NP = RSU * G / 2;  // accumulator pairs per token (RSU * G is even)
+    static_assert(RSU * G % 2 == 0, "phase-1 accumulators are updated in pairs");
     for (int j0 = 0; j0 < rows_s; j0 += RSU) {
-      float acc[RSU * G * TT];
+      float2 accp[NP][TT];
 #pragma unroll
-      for (int i = 0; i < RSU * G * TT; ++i) acc[i] = 0.f;
+      for (int q = 0; q < NP; ++q)
+#pragma unroll
+        for (int t = 0; t < TT; ++t) accp[q][t] = make_float2(0.f, 0.f);
       const bool live1 = RSU > 1 && j0 + 1 < rows_s;
 #pragma unroll 2
       for (int k = kb + lane * VE; k < ke; k += STEP) {
@@ -371,6 +378,11 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
                            ? *reinterpret_cast<const uint4*>(st + (size_t(m) * fp.rs_up + j0 + j) * row1 +
                                                              size_t(k) * sizeof(WT))
                            : make_uint4(0, 0, 0, 0);
+        float wf[RSU * G][VE];  // index j * G + m
+#pragma unroll
+        for (int j = 0; j < RSU; ++j)
+#pragma unroll
+          for (int m = 0; m < G; ++m) unpack<WT>(wv[j][m], wf[j * G + m]);
         const int pos = xs_pos<WT>(k, p.kt);
 #pragma unroll
         for (int t = 0; t < TT; ++t) {
@@ -383,17 +395,21 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
             xv[4] = b.x; xv[5] = b.y; xv[6] = b.z; xv[7] = b.w;
           }
 #pragma unroll
-          for (int j = 0; j < RSU; ++j)
+          for (int q = 0; q < NP; ++q)
 #pragma unroll
-            for (int m = 0; m < G; ++m) {
-              float wf[VE];
-              unpack<WT>(wv[j][m], wf);
-              float& a_ = acc[(j * G + m) * TT + t];
-#pragma unroll
-              for (int e = 0; e < VE; ++e) a_ = fmaf(wf[e], xv[e], a_);
-            }
+            for (int e = 0; e < VE; ++e)
+              accp[q][t] = __ffma2_rn(make_float2(xv[e], xv[e]), make_float2(wf[2 * q][e], wf[2 * q + 1][e]),
+                                      accp[q][t]);
         }
       }
+      float acc[RSU * G * TT];  // (j * G + m) * TT + t
+#pragma unroll
+      for (int q = 0; q < NP; ++q)
+#pragma unroll
+        for (int t = 0; t < TT; ++t) {
+          acc[(2 * q) * TT + t] = accp[q][t].x;
+          acc[(2 * q + 1) * TT + t] = accp[q][t].y;
+        }
       constexpr int CNT = RSU * G * TT;
       constexpr int LOGC = CNT == 1 ? 0 : CNT == 2 ? 1 : CNT == 4 ? 2 : CNT == 8 ? 3 : CNT == 16 ? 4 : 5;
       const float r = warp_reduce_transposed<CNT>(acc, lane);
@@ -429,13 +445,15 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
   // ---- phase 2: y_c[t, :] = sum_h a[t, h] * W2[h, :] ----
   const int tid = threadIdx.x;
   const int n_vec = (p.N + VE - 1) / VE;
-  float acc2[NV][VE][TT];
+  // column pairs (e, e + 1) updated by packed FFMA2 with a[t, h] broadcast (per
+  // accumulator the same fma sequence as scalar FFMAs)
+  float2 acc2[NV][VE / 2][TT];
 #pragma unroll
   for (int v = 0; v < NV; ++v)
 #pragma unroll
-    for (int e = 0; e < VE; ++e)
+    for (int e = 0; e < VE / 2; ++e)
 #pragma unroll
-      for (int t = 0; t < TT; ++t) acc2[v][e][t] = 0.f;
+      for (int t = 0; t < TT; ++t) acc2[v][e][t] = make_float2(0.f, 0.f);
   for (int d = 0; d < n_dn; ++d) {
     const int s = n_up + d;
     const int slot = s % NST;
@@ -455,9 +473,11 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
           float wf[VE];
           unpack<WT>(w, wf);
 #pragma unroll
-          for (int e = 0; e < VE; ++e)
+          for (int e = 0; e < VE / 2; ++e)
 #pragma unroll
-            for (int t = 0; t < TT; ++t) acc2[v][e][t] = fmaf(wf[e], at[t], acc2[v][e][t]);
+            for (int t = 0; t < TT; ++t)
+              acc2[v][e][t] = __ffma2_rn(make_float2(at[t], at[t]), make_float2(wf[2 * e], wf[2 * e + 1]),
+                                         acc2[v][e][t]);
         }
       }
     }
@@ -480,11 +500,11 @@ __global__ void __launch_bounds__(kBlockThreads, 1) ffn_block_kernel(const __gri
 #pragma unroll
         for (int e = 0; e < VE; e += 4)
           *reinterpret_cast<float4*>(orow + n0 + e) =
-              make_float4(acc2[v][e][t], acc2[v][e + 1][t], acc2[v][e + 2][t], acc2[v][e + 3][t]);
+              make_float4(acc2[v][e / 2][t].x, acc2[v][e / 2][t].y, acc2[v][e / 2 + 1][t].x, acc2[v][e / 2 + 1][t].y);
       } else {
 #pragma unroll
         for (int e = 0; e < VE; ++e)
-          if (n0 + e < p.N) orow[n0 + e] = acc2[v][e][t];
+          if (n0 + e < p.N) orow[n0 + e] = (e & 1) ? acc2[v][e / 2][t].y : acc2[v][e / 2][t].x;
       }
     }
   }
