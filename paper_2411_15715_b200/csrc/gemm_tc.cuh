@@ -69,6 +69,10 @@ struct GemmArgs {
   float* partial;
   int* tickets;
   int dbg_no_mma;  // probe: stream the operands but issue no MMA (SP_TC_DBG_NOMMA)
+  // trace: atomicMin of every CTA's start / atomicMax of every CTA's end
+  // (%globaltimer ns) over the block's chain, or null
+  unsigned long long* kspan0;
+  unsigned long long* kspan1;
 };
 
 // Programmatic dependent launch (PDL).  The prefill chain gather -> up GEMM ->
@@ -158,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (g.kspan0 && threadIdx.x == 0) atomicMin(g.kspan0, global_ns());
   // blockIdx -> (token tile, row tile, split)
   const int ks_id = blockIdx.x % g.ks;
   const int tile = blockIdx.x / g.ks;  // = mt * t_tiles + tt
@@ -423,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (g.kspan1 && threadIdx.x == 0) atomicMax(g.kspan1, global_ns());
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
@@ -501,6 +507,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (g.kspan0 && threadIdx.x == 0) atomicMin(g.kspan0, global_ns());
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
   const int ks_id = pair % g.ks;
@@ -629,6 +636,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();  // the peer's MMAs / barrier traffic are over before either rank frees or exits
+  if (g.kspan1 && threadIdx.x == 0) atomicMax(g.kspan1, global_ns());
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
@@ -665,8 +673,10 @@ __global__ void swiglu_reduce_kernel(const float* __restrict__ z, int ks, int na
 // gather x rows (any dtype) into a contiguous bf16 [T, ldo] buffer; `vec`: 8 elements
 // per thread with 16-byte (bf16) / 2 x 16-byte (f32) loads (rows 16-byte aligned)
 __global__ void gather_rows_bf16_kernel(const void* x, int xdtype, int64_t ldx_in, const int32_t* ids, int t0,
-                                        int T, int M, __nv_bfloat16* out, int64_t ldo, int vec) {
+                                        int T, int M, __nv_bfloat16* out, int64_t ldo, int vec,
+                                        unsigned long long* kspan0) {
   grid_dep_launch();  // the up GEMM starts streaming its weights meanwhile
+  if (kspan0 && threadIdx.x == 0) atomicMin(kspan0, global_ns());
   const int t = blockIdx.y;
   if (t >= T) return;
   const int64_t row = ids ? ids[t0 + t] : int64_t(t0 + t);

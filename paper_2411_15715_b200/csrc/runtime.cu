@@ -633,6 +633,7 @@ struct CallWs {
   float* ycc;      // [T_e, N] CC partial (from the host)
   int32_t* ids;    // device
   float* gates;    // device
+  bool ids_identity = false;  // the call's tokens are rows 0..T_e-1 of x (no token_ids)
 };
 
 // ---- tensor-core (tcgen05) block path for many tokens -------------------------
@@ -838,7 +839,9 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
                         CallWs& w, const int32_t* dev_ids, int64_t T_e, int t0, int T, cudaStream_t s,
                         bool resident) {
   const int64_t M = L->d.model_dim, N = L->d.out_dim, R = b.rows;
-  if (w.tc_slice < 0) {
+  // streamed chunks accumulate into one shared slice (zeroed once per call);
+  // a resident block stores its own split slices, so its chain starts with the gather
+  if (!resident && w.tc_slice < 0) {
     w.tc_slice = w.S++;
     SP_CUDA(cudaMemsetAsync(w.part + size_t(w.tc_slice) * T_e * N, 0, size_t(T_e) * N * 4, s));
   }
@@ -891,21 +894,34 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
     dn.ks = 1;  // streamed chunk: hidden under its copy, accumulate into the tc slice
     dn.y = w.part + size_t(w.tc_slice) * T_e * N + size_t(t0) * N;
   }
+  if (C->trace.kslot_cur >= 0) {  // the block's chain span (trace ABI dev_s)
+    up.kspan0 = dn.kspan0 = C->trace.kspan + C->trace.kslot_cur;
+    up.kspan1 = dn.kspan1 = C->trace.kspan + kKSlots + C->trace.kslot_cur;
+  }
+  // bf16 x whose tokens are its own rows in order feeds the up GEMM's TMA
+  // directly (out-of-range columns / rows read as zero); otherwise the gather
+  // kernel builds the bf16 token tile first
+  static const bool direct_x_env = env_int("SP_TC_DIRECT_X", 1) != 0;
+  const bool x_direct = direct_x_env && w.ids_identity && xdtype == SP_BF16 && (size_t(ldx) * 2) % 16 == 0 &&
+                        reinterpret_cast<uintptr_t>(x) % 16 == 0;
+  const void* xt = x_direct ? static_cast<const void*>(static_cast<const char*>(x) + size_t(t0) * ldx * 2)
+                            : static_cast<const void*>(w.x_tc);
+  const int64_t xt_stride = x_direct ? ldx * 2 : L->ldm * 2;
   CUtensorMap tx, tw1, tw3, ta, tw2;
   SP_TRY(make_tmap(&tw1, b.base, M, R, L->ldm * 2, tc::BK, tc::BM));
   SP_TRY(make_tmap(&tw3, L->d.gated ? b.base + b.w3_off : b.base, M, R, L->ldm * 2, tc::BK, tc::BM));
-  SP_TRY(make_tmap(&tx, w.x_tc, M, T, L->ldm * 2, tc::BK, nt));
+  SP_TRY(make_tmap(&tx, xt, M, T, xt_stride, tc::BK, nt));
   SP_TRY(make_tmap(&tw2, b.base + b.w2_off, N, R, L->ldn * 2, 64, tc::BK));
   SP_TRY(make_tmap(&ta, w.a_tc, R, T, w.ld_a * 2, tc::BK, nt));
 
   // gathered bf16 x rows [T, M]
-  {
+  if (!x_direct) {
     const size_t xel = xdtype == SP_BF16 ? 2 : 4;
     const bool vec = M % 8 == 0 && (size_t(ldx) * xel) % 16 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0;
     const int per = vec ? 8 : 1;
     dim3 grid(unsigned(std::min<int64_t>((M / per + 255) / 256, 16)), unsigned(T));
     tc::gather_rows_bf16_kernel<<<grid, 256, 0, s>>>(x, xdtype, ldx, dev_ids, t0, T, int(M), w.x_tc, L->ldm,
-                                                     vec ? 1 : 0);
+                                                     vec ? 1 : 0, up.kspan0);
     SP_CUDA(cudaGetLastError());
     ++C->launches;
   }
@@ -914,15 +930,15 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
     // Measured (ncu, 14336-row expert): T = 512 up GEMM 153 -> 141 us, T = 256
     // expert 134 -> 129 us; at 64/128-token tiles it was within +-4 % either way.
     CUtensorMap txh;
-    SP_TRY(make_tmap(&txh, w.x_tc, M, T, L->ldm * 2, tc::BK, nt / 2));
+    SP_TRY(make_tmap(&txh, xt, M, T, xt_stride, tc::BK, nt / 2));
     if (L->d.gated)
-      SP_TRY((launch_gemm_pair<2>(C, nt, tw1, tw3, txh, up, s, true)));
+      SP_TRY((launch_gemm_pair<2>(C, nt, tw1, tw3, txh, up, s, !x_direct)));
     else
-      SP_TRY((launch_gemm_pair<1>(C, nt, tw1, tw1, txh, up, s, true)));
+      SP_TRY((launch_gemm_pair<1>(C, nt, tw1, tw1, txh, up, s, !x_direct)));
   } else if (L->d.gated) {
-    SP_TRY((launch_gemm<2, false>(C, nt, tw1, tw3, tx, up, s, true)));
+    SP_TRY((launch_gemm<2, false>(C, nt, tw1, tw3, tx, up, s, !x_direct)));
   } else {
-    SP_TRY((launch_gemm<1, false>(C, nt, tw1, tw1, tx, up, s, true)));
+    SP_TRY((launch_gemm<1, false>(C, nt, tw1, tw1, tx, up, s, !x_direct)));
   }
   if (up.ks > 1) {
     dim3 grid(unsigned((R / 4 + 127) / 128 + 1), unsigned(T));
@@ -1345,6 +1361,7 @@ static int forward_batch(Context* C, const sp_call* calls, int n_calls, const vo
     }
     ws[c].ycc = reinterpret_cast<float*>(dws + o_ycc[c]);
     ws[c].ids = reinterpret_cast<int32_t*>(dmeta + size_t(meta_off) * 8);
+    ws[c].ids_identity = calls[c].token_ids == nullptr;
     ws[c].gates = reinterpret_cast<float*>(dmeta + size_t(meta_off) * 8 + size_t(calls[c].tokens) * 4);
     meta_off += calls[c].tokens;
   }

@@ -24,7 +24,7 @@ scratch = torch.zeros(64 << 20, device="cuda")
 import os
 for T in [int(t) for t in os.environ.get("SP_PREFILL_T", "16 64 128 256 512").split()]:
     x = torch.randn(T, M, device="cuda").to(torch.bfloat16)
-    ts = []
+    ts, ds = [], []
     for r in range(6):
         scratch.sum()  # L2 flush by reading: a write would leave dirty lines whose write-back competes
         torch.cuda.synchronize()
@@ -34,7 +34,11 @@ for T in [int(t) for t in os.environ.get("SP_PREFILL_T", "16 64 128 256 512").sp
         nat.trace_enable(False)
         if r >= 2:
             ts.append(sp[0]["end_s"] - sp[0]["start_s"])
+            ds.append(sp[0].get("dev_s", 0.0))
     t = float(np.median(ts))
+    d = float(np.median(ds))
     flops = 2.0 * T * 3 * M * H
     print(f"H={H} T={T}: {t*1e6:8.1f} us  {flops/t/1e12:7.1f} TFLOP/s ({flops/t/1e12/peaks.get('bf16_tflops', 1669):.3f} of bf16 peak)"
-          f"  weights {nbytes/t/1e9:7.0f} GB/s ({nbytes/t/1e9/peaks.get('hbm_gbs', 6550):.3f} of HBM)", flush=True)
+          f"  weights {nbytes/t/1e9:7.0f} GB/s ({nbytes/t/1e9/peaks.get('hbm_gbs', 6550):.3f} of HBM)"
+          + (f"  | device span {d*1e6:6.1f} us ({nbytes/d/1e9/peaks.get('hbm_gbs', 6550):.3f} of HBM)" if d > 0 else ""),
+          flush=True)
