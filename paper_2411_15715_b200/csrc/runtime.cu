@@ -816,13 +816,14 @@ static int launch_gemm_pair(Context* C, int nt, const CUtensorMap& a0, const CUt
     case 128: return launch_gemm_pair_t<128, NA>(C, a0, a1, b, g, s, pdl);
     case 64: return launch_gemm_pair_t<64, NA>(C, a0, a1, b, g, s, pdl);
     case 32: return launch_gemm_pair_t<32, NA>(C, a0, a1, b, g, s, pdl);
+    case 16: return launch_gemm_pair_t<16, NA>(C, a0, a1, b, g, s, pdl);
     default: return fail(SP_ERR_VALUE, "CTA-pair up GEMM: no %d-token tile", nt);
   }
 }
 // SP_TC_PAIR=0 keeps every up GEMM on single-CTA tiles
 static const bool g_tc_pair = env_int("SP_TC_PAIR", 1) != 0;
 // smallest token tile that runs the up GEMM on CTA pairs (SP_TC_PAIR_MIN_NT)
-static const int g_tc_pair_min_nt = env_int("SP_TC_PAIR_MIN_NT", 32);
+static const int g_tc_pair_min_nt = env_int("SP_TC_PAIR_MIN_NT", 16);
 
 // Split K so the launch puts ~`target` CTAs to work (bounded by the k-blocks).
 static int split_k(int tiles, int k, int target) {
@@ -925,11 +926,12 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
     SP_CUDA(cudaGetLastError());
     ++C->launches;
   }
-  if (g_tc_pair && nt >= std::max(32, g_tc_pair_min_nt)) {
+  if (g_tc_pair && nt >= std::max(16, g_tc_pair_min_nt)) {
     // x tile split across the two SMs of a CTA pair: fewer bytes into each SM.
     // Measured (ncu, 14336-row expert): T = 512 up GEMM 153 -> 141 us, T = 256
     // expert 134 -> 129 us; with x read by the TMA map directly, 64 / 128-token
-    // tiles -3.5 / -4.6 % (profiles/r2/tc_pair_small_ab.txt).
+    // tiles -3.5 / -4.6 %, 16-token tiles -5 % (60 vs 63 us device span;
+    // profiles/r2/tc_pair_small_ab.txt).
     CUtensorMap txh;
     SP_TRY(make_tmap(&txh, xt, M, T, xt_stride, tc::BK, nt / 2));
     if (L->d.gated)
