@@ -643,172 +643,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
-// ---- down GEMM on CTA pairs -----------------------------------------------------
-//
-// D[n, t] = W2[:, n] . a[t, :] with M = 256 output columns per MMA across the
-// pair: rank r of pair p holds columns n0 + 256 a + 128 r of each of its NA
-// sub-tiles (two 64-column MN-major boxes per sub-tile, as gemm_kernel<.., true>)
-// and HALF of the `a` tile (tokens t0 + r * NT/2); the tensor cores read the
-// peer's half over the pair.  Each rank stores (split_slices) or accumulates
-// (ks == 1) its own 128 columns per sub-tile, exactly as gemm_kernel does.
-// grid: 2 * m_tiles * t_tiles * ks CTAs, cluster (2, 1, 1); m_tiles counts
-// NA * 256-column pair tiles.
-template <int NT, int NA>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_down_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                          const GemmArgs g) {
-  constexpr int HALF = NT / 2;
-  constexpr int A_BYTES = BM * BK * 2;  // 16 KB: this rank's 128 columns x BK rows
-  constexpr int B_BYTES = HALF * BK * 2;
-  constexpr int STAGE = NA * A_BYTES + B_BYTES;
-  constexpr int TMEM_COLS = (NA * NT) <= 32 ? 32 : (NA * NT) <= 64 ? 64 : (NA * NT) <= 128 ? 128
-                            : (NA * NT) <= 256 ? 256 : 512;
-  static_assert(HALF % 8 == 0, "a half-tile must be whole 8-row swizzle atoms");
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int S = g.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(S) * STAGE);
-  uint64_t* empty = full + S;
-  uint64_t* tmem_full = empty + S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (g.kspan0 && threadIdx.x == 0) atomicMin(g.kspan0, global_ns());
-  const uint32_t rank = cluster_ctarank();
-  const int pair = blockIdx.x >> 1;
-  const int ks_id = pair % g.ks;
-  const int tp = pair / g.ks;  // = mt * t_tiles + tt
-  const int mt = tp / g.t_tiles, tt = tp % g.t_tiles;
-  const int n0 = mt * NA * 2 * BM + int(rank) * BM, t0 = tt * NT;  // this rank's column of sub-tile 0
-  const int nkb = (g.k + BK - 1) / BK;
-  const int kb0 = nkb * ks_id / g.ks, kb1 = nkb * (ks_id + 1) / g.ks;
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(tmem_full, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  cluster_sync_all();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-
-  const int nk = kb1 - kb0;
-  grid_dep_launch();
-  if (warp == 0) {
-    if (lane == 0) {
-      auto load_a = [&](int i) {
-        const int kb = kb0 + i, s = i % S;
-        unsigned char* st = smem + size_t(s) * STAGE;
-        const uint32_t lbar = map_to_rank(&full[s], 0);
-#pragma unroll
-        for (int a = 0; a < NA; ++a) {
-          const int na0 = n0 + a * 2 * BM;
-          tma_load_2d_pair(st + a * A_BYTES, &tmA, lbar, na0, kb * BK);
-          tma_load_2d_pair(st + a * A_BYTES + BK * 128, &tmA, lbar, na0 + 64, kb * BK);
-        }
-      };
-      auto load_b = [&](int i) {
-        const int kb = kb0 + i, s = i % S;
-        tma_load_2d_pair(smem + size_t(s) * STAGE + NA * A_BYTES, &tmB, map_to_rank(&full[s], 0), kb * BK,
-                         t0 + int(rank) * HALF);
-      };
-      const int pre = nk < S ? nk : S;
-      for (int i = 0; i < pre; ++i) {
-        if (rank == 0) mbar_expect_tx(&full[i], 2 * STAGE);
-        load_a(i);
-      }
-      grid_dep_wait();
-      for (int i = 0; i < pre; ++i) load_b(i);
-      for (int i = pre; i < nk; ++i) {
-        const int s = i % S;
-        mbar_wait(&empty[s], ((i / S) - 1) & 1);
-        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE);
-        load_a(i);
-        load_b(i);
-      }
-    }
-  } else if (warp == 1) {
-    if (rank == 0) {
-      const uint32_t idesc = umma_idesc(2 * BM, NT, true);
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % S;
-        mbar_wait(&full[s], (i / S) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (lane == 0) {
-          const unsigned char* st = smem + size_t(s) * STAGE;
-#pragma unroll
-          for (int kk = 0; kk < BK / UK; ++kk) {
-            const uint64_t b = umma_desc(st + NA * A_BYTES + kk * 32, 16, 1024);
-#pragma unroll
-            for (int a = 0; a < NA; ++a)
-              umma_bf16_pair(tmem + uint32_t(a * NT), umma_desc(st + a * A_BYTES + kk * UK * 128, BK * 128, 1024), b,
-                             idesc, (i > 0 || kk > 0) ? 1u : 0u);
-          }
-          umma_commit_pair(&empty[s]);
-          if (i == nk - 1) umma_commit_pair(tmem_full);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16);
-    float* ys = g.split_slices ? g.y + int64_t(ks_id) * g.y_split_stride : g.y;
-    grid_dep_wait();
-    if (kb1 > kb0) {
-      mbar_wait(tmem_full, 0);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
-#pragma unroll 1
-    for (int c = 0; c < NT; c += 16) {
-      uint32_t r[NA][16];
-#pragma unroll
-      for (int a = 0; a < NA; ++a) {
-        if (kb1 > kb0) {
-          tmem_ld16(lane_addr + uint32_t(a * NT + c), r[a]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) r[a][e] = 0u;
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int t = t0 + c + e;
-        if (t >= g.T) break;
-#pragma unroll
-        for (int a = 0; a < NA; ++a) {
-          const int mm = n0 + a * 2 * BM + row;
-          if (mm >= g.rows) continue;
-          if (g.split_slices)
-            ys[int64_t(t) * g.ldy + mm] = __uint_as_float(r[a][e]);
-          else
-            ys[int64_t(t) * g.ldy + mm] += __uint_as_float(r[a][e]);
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  cluster_sync_all();
-  if (g.kspan1 && threadIdx.x == 0) atomicMax(g.kspan1, global_ns());
-  if (warp == 1) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
-  }
-}
-
 // a[t, h] = act(sum_q z[q][0][t][h]) [* sum_q z[q][1][t][h]], splits summed in order
 __global__ void swiglu_reduce_kernel(const float* __restrict__ z, int ks, int na, int T, int R, int64_t zld,
                                      int act, __nv_bfloat16* __restrict__ a_out, int64_t lda) {

@@ -820,37 +820,6 @@ static int launch_gemm_pair(Context* C, int nt, const CUtensorMap& a0, const CUt
     default: return fail(SP_ERR_VALUE, "CTA-pair up GEMM: no %d-token tile", nt);
   }
 }
-// down GEMM on CTA pairs (gemm_down_pair_kernel): g.m_tiles counts NA * 256-column pair tiles
-template <int NT, int NA>
-static int launch_gemm_down_pair_t(Context* C, const CUtensorMap& a, const CUtensorMap& b, tc::GemmArgs g,
-                                   cudaStream_t s, bool pdl) {
-  auto kern = tc::gemm_down_pair_kernel<NT, NA>;
-  constexpr int STAGE = NA * tc::BM * tc::BK * 2 + (NT / 2) * tc::BK * 2;
-  static bool attr_set = false;
-  if (!attr_set) {
-    SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-    attr_set = true;
-  }
-  g.stages = std::max(2, std::min(6, (kSmemLimit - 1024 - 256) / STAGE));
-  const size_t smem = size_t(g.stages) * STAGE + 1024 + 256;
-  SP_CUDA(launch_k(kern, dim3(2 * g.m_tiles * g.t_tiles * g.ks), dim3(tc::kThreads), smem, s, pdl, a, b, g));
-  ++C->launches;
-  return SP_OK;
-}
-
-template <int NA>
-static int launch_gemm_down_pair(Context* C, int nt, const CUtensorMap& a, const CUtensorMap& b,
-                                 const tc::GemmArgs& g, cudaStream_t s, bool pdl) {
-  switch (nt) {
-    case 16: return launch_gemm_down_pair_t<16, NA>(C, a, b, g, s, pdl);
-    case 32: return launch_gemm_down_pair_t<32, NA>(C, a, b, g, s, pdl);
-    case 64: return launch_gemm_down_pair_t<64, NA>(C, a, b, g, s, pdl);
-    case 128: return launch_gemm_down_pair_t<128, NA>(C, a, b, g, s, pdl);
-    default: return launch_gemm_down_pair_t<256, NA>(C, a, b, g, s, pdl);
-  }
-}
-// SP_TC_DOWN_PAIR=1: the down GEMM on CTA pairs as well (probe)
-static const bool g_tc_down_pair = env_int("SP_TC_DOWN_PAIR", 0) != 0;
 // SP_TC_PAIR=0 keeps every up GEMM on single-CTA tiles
 static const bool g_tc_pair = env_int("SP_TC_PAIR", 1) != 0;
 // smallest token tile that runs the up GEMM on CTA pairs (SP_TC_PAIR_MIN_NT)
@@ -979,15 +948,6 @@ static int run_block_tc(Context* C, const sp_layer* L, const BlockView& b, const
     SP_CUDA(launch_k(tc::swiglu_reduce_kernel, grid, dim3(128), 0, s, true, static_cast<const float*>(up.z), up.ks,
                      na, T, int(R), up.zld, int(L->d.act), w.a_tc, w.ld_a));
     ++C->launches;
-  }
-  if (g_tc_down_pair) {
-    // pair tiles of 2 * sub * 128 columns; the same splits as the single-CTA tiles
-    // (dn.ks was sized for dn.m_tiles single tiles, i.e. 2 CTAs per pair tile)
-    tc::GemmArgs dp = dn;
-    dp.m_tiles = int((N + 2 * tc::BM * sub - 1) / (2 * tc::BM * sub));
-    CUtensorMap tah;
-    SP_TRY(make_tmap(&tah, w.a_tc, R, T, w.ld_a * 2, tc::BK, nt / 2));
-    return launch_gemm_down_pair<sub>(C, nt, tw2, tah, dp, s, true);
   }
   return launch_gemm<sub, true>(C, nt, tw2, tw2, ta, dn, s, true);
 }
