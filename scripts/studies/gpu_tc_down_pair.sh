@@ -1,4 +1,5 @@
 #!/bin/bash
+# (the kernel and the SP_TC_DOWN_PAIR switch exist only at commit 475dfe0)
 # down GEMM on CTA pairs (SP_TC_DOWN_PAIR=1): parity first (bounded), then the one-expert chain, alternating
 mkdir -p gpurun_out/dp
 F=gpurun_out/dp/ab.txt
