@@ -987,6 +987,13 @@ def run_prefill_decode(args):
     nat.trace_enable(False)
     ycc = [s for s in pspans if s["kind"] == "ycc"]
     ycc_meas = sum(s["end_s"] - s["start_s"] for s in ycc) / args.layers
+    # the GG blocks of the traced prefill: tcgen05 chains (~128 tokens per expert)
+    ggs = [s for s in pspans if s["kind"] == "gg" and s["bytes"] > 0]
+    gg_b = sum(s["bytes"] for s in ggs)
+    gg_t = sum(s["end_s"] - s["start_s"] for s in ggs)
+    gg_d = sum(s["dev_s"] for s in ggs if s["dev_s"] > 0)
+    peaks_doc = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = peaks_doc.get("hbm_gbs")
     ycc_model = sum(sp.cc_result_transfer_time(p_profile, layer_spec,
                                                sp.Workload(tokens=len(c.token_ids) - c.n_g, phase=sp.Phase.PROMPT),
                                                rates, bytes_per_activation=4.0)
@@ -1035,6 +1042,18 @@ def run_prefill_decode(args):
         "e2e": {"value": args.prompt / t_e2e, "unit": UNIT, "h2d_bytes_per_step": args.prompt * args.model_dim * 2 * args.layers,
                 "d2h_bytes_per_step": args.prompt * args.model_dim * 4 * args.layers},
         "gpu_launches": launches, "clocks": clk.summary(), "prompt_calibration": pcalib,
+        "roofline": {"bound": "hbm", "kernel": "tcgen05 GG chains (CTA-pair up GEMM + down GEMM) of one traced prefill",
+                     "achieved": gg_b / gg_t / 1e9 if gg_t else None, "peak": hbm, "unit": "GB/s",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else None,
+                     "frac": gg_b / gg_t / 1e9 / hbm if gg_t and hbm else None, "traffic": None,
+                     "algorithmic_bytes_per_launch": gg_b / len(ggs) if ggs else None,
+                     "mean_launch_us": gg_t / len(ggs) * 1e6 if ggs else None,
+                     "frac_device_span": gg_b / gg_d / 1e9 / hbm if gg_d and hbm else None,
+                     "blocks": len(ggs),
+                     "timing": "per GG block: CUDA events on the compute stream (frac) and the chain's in-kernel "
+                               "%globaltimer span (frac_device_span); the GG work is ~2 % of a prefill layer, its blocks "
+                               "(half an expert, ~128 tokens, split K) share the SMs with the CG chunk kernels and "
+                               "their events sit under a saturated host link"},
         "ycc_transfer": {"measured_ms_per_layer": ycc_meas * 1e3,
                          "model_ms_per_layer": ycc_model * 1e3 if ycc_model is not None else None,
                          "note": "CC partials host->HBM (pipeline.py:367-383 cc_result_transfer_time, fp32 "
